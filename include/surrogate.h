@@ -1,0 +1,184 @@
+/*
+ * surrogate.h — C ABI of the B200 (sm_100a) exhaustive FCNN-surrogate sweep.
+ *
+ * The method (arxiv 2306.14011): a fully connected ReLU network predicts the
+ * solver runtime of a SENSEI configuration from its 14 OpenACC scheduling
+ * parameters (7 kernels x {gang, vector}, Table "Tuning
+ * Parameters" PAPER.md:253-266), after StandardScaler feature scaling
+ * (PAPER.md:271-273).  The paper only says the trained model "identifies
+ * configurations with the lowest runtime"; this library does
+ * that exhaustively: every flat index of the space is mixed-radix decoded,
+ * normalised, pushed through the network on tcgen05 tensor cores and reduced
+ * to the k fastest predicted configurations.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns surr_status; nothing throws across the ABI.  On error
+ *    no output is written and surrogate_last_error() holds the reason.
+ *  - Arguments are validated before any launch.
+ *  - Input descriptors (surr_space, surr_model and the arrays they point to)
+ *    are HOST memory owned by the caller and copied during the call.
+ *  - Outputs named *_dev are caller-allocated DEVICE buffers on the handle's
+ *    device; *_host outputs are host memory.  Calls taking `stream` (a
+ *    cudaStream_t, NULL = legacy default stream) are stream-ordered and
+ *    asynchronous unless the name says _host.
+ *  - A handle is not thread-safe; distinct handles are independent.
+ *  - There is no CPU fallback: without an sm_100 device every call that needs
+ *    the GPU returns SURR_E_NO_DEVICE.
+ */
+#ifndef PAPER_2306_14011_SURROGATE_H
+#define PAPER_2306_14011_SURROGATE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct surrogate surrogate_t; /* opaque; owns every device buffer it allocates */
+
+typedef enum {
+  SURR_OK = 0,
+  SURR_E_INVALID_ARG = 1, /* null pointer, bad shape, k == 0 or k > SURR_K_MAX, begin > end ... */
+  SURR_E_RANGE = 2,       /* |S| >= 2^64, or an index split the decoder cannot represent */
+  SURR_E_NO_DEVICE = 3,   /* no CUDA device, or the device is not sm_100 */
+  SURR_E_CUDA = 4,        /* a CUDA runtime error (text in surrogate_last_error) */
+  SURR_E_OOM = 5,         /* device or pinned-host allocation failed */
+  SURR_E_NOT_LOADED = 6,  /* no model loaded on this handle */
+  SURR_E_UNSUPPORTED = 7  /* shape outside the kernel envelope (widths, layers, params) */
+} surr_status;
+
+/* Arithmetic of the hidden layers.  The final H -> 1 layer and the
+ * de-standardisation always run in FP32 on CUDA cores. */
+typedef enum {
+  SURR_PREC_BF16 = 0, /* BF16 operands, FP32 accumulate (tcgen05 kind::f16) */
+  SURR_PREC_FP32 = 1, /* "FP32 path": 3xTF32 split (hi*hi + hi*lo + lo*hi), kind::tf32 */
+  SURR_PREC_TF32 = 2  /* 1xTF32 hidden layers, 3xTF32 first layer */
+} surr_precision;
+
+#define SURR_K_MAX 1024u        /* largest top-k */
+#define SURR_MAX_PARAMS 30u     /* tuning parameters per config (paper: 14) */
+#define SURR_MAX_HIDDEN_LAYERS 4u
+
+/* Search-space descriptor (Table "Tuning Parameters").
+ * Flat index I = sum_j d_j * prod_{l>j} r_l with parameter 0 most significant
+ * (lexicographic order of value indices).  [begin, end) selects a
+ * sub-range; end == 0 means |S|.  */
+typedef struct {
+  uint32_t num_params;  /* P, 1..SURR_MAX_PARAMS */
+  const uint32_t *radix; /* [P] value-list lengths r_j >= 1 */
+  const double *values;  /* concatenated value lists, sum_j r_j entries, list j strictly increasing */
+  uint64_t begin, end;   /* index sub-range; end == 0 -> |S| */
+} surr_space;
+
+/* A trained FCNN, or an ensemble of E members with
+ * identical widths whose predictions are averaged in seconds.
+ * widths[0] = F = P + num_const_features, widths[1..L-1] = hidden width H
+ * (all equal), widths[L] = 1.  W[e*L + l] is row-major fan_in x fan_out,
+ * b[e*L + l] has fan_out entries.  The input transform is
+ * z = (x - x_shift) / x_scale (StandardScaler: shift = mean, scale = population
+ * std; min-max: shift = min, scale = max - min);
+ * x_scale == 0 is treated as 1.  The output is t = y_mean + y_scale * yhat
+ * (SURVEY G4).  Constant device features are raw
+ * values appended after the P tuning parameters; they are folded into the
+ * first-layer bias at load time.  Current kernel envelope: E == 1,
+ * H in {32, 64, 128}, 1 <= L-1 <= SURR_MAX_HIDDEN_LAYERS, P + 1 <= 32. */
+typedef struct {
+  uint32_t num_layers;           /* L affine layers */
+  const uint32_t *widths;        /* [L + 1] */
+  const double *const *W;        /* [E * L] */
+  const double *const *b;        /* [E * L] */
+  const double *x_shift;         /* [F] */
+  const double *x_scale;         /* [F] */
+  double y_mean, y_scale;        /* (0, 1) = identity */
+  uint32_t num_const_features;   /* F - P */
+  const double *const_features;  /* [F - P] raw values, or NULL when 0 */
+  uint32_t ensemble;             /* E >= 1 */
+  surr_precision precision;
+} surr_model;
+
+/* One result record as written by the sweep kernels: the k best of a
+ * sub-range, sorted ascending by (t, idx); NaN ranks after +inf; unused
+ * slots hold the sentinel (idx = UINT64_MAX, key = 0xFFFFFFFF). key is the
+ * order-preserving uint32 image of the float time. */
+typedef struct {
+  uint64_t idx;
+  uint32_t key;
+  uint32_t pad;
+} surr_record;
+
+/* Create a handle on CUDA device `cuda_device` (must be sm_100). */
+surr_status surrogate_create(int cuda_device, surrogate_t **out);
+void surrogate_destroy(surrogate_t *h);
+const char *surrogate_last_error(const surrogate_t *h);
+
+/* Validate the model against the kernel envelope, fold constant features, b_1,
+ * y_mean / y_scale into the layer parameters, convert to the precision's
+ * operand format, pack the UMMA shared-memory image (K-major, no swizzle) and
+ * upload it (synchronous).  PAPER.md:54, :63, :273. */
+surr_status surrogate_load_weights(surrogate_t *h, const surr_model *model);
+
+/* Predict an explicit batch: x_dev holds n rows of P raw parameter values
+ * (row-major float32, device); t_dev receives n predicted times in seconds.
+ * Row-wise pure.  n == 0 is a no-op. */
+surr_status surrogate_predict(surrogate_t *h, const float *x_dev, uint64_t n, float *t_dev, void *stream);
+
+/* Exhaustive sweep of [begin, end): the k smallest (t, I), sorted.
+ * idx_dev[k], t_dev[k]; *count_host = min(k, end - begin).
+ * k in 1..SURR_K_MAX.  The space's value lookup table is cached on the
+ * handle and re-uploaded only when the descriptor changes. */
+surr_status surrogate_sweep(surrogate_t *h, const surr_space *space, uint32_t k, uint64_t *idx_dev, float *t_dev,
+                            uint32_t *count_host, void *stream);
+
+/* The same sweep end to end with HOST outputs: rebuilds and uploads the value
+ * table, runs the sweep and copies the k results back; synchronous. */
+surr_status surrogate_sweep_host(surrogate_t *h, const surr_space *space, uint32_t k, uint64_t *idx_host,
+                                 float *t_host, uint32_t *count_host, void *stream);
+
+/* Parity hook: the fused sweep kernel in dense-output mode writes t(I) for
+ * every I in [begin, end) to t_dev[I - begin]. */
+surr_status surrogate_eval_range(surrogate_t *h, const surr_space *space, float *t_dev, void *stream);
+
+/* Merge `lists` sorted record lists of k_in entries each (device, contiguous)
+ * into the k best, sorted (used after the NCCL
+ * allgather).  k <= k_in * lists is not required: short results are padded
+ * with sentinels. */
+surr_status surrogate_merge_topk(surrogate_t *h, const surr_record *recs_dev, uint32_t lists, uint32_t k_in,
+                                 uint32_t k, uint64_t *idx_dev, float *t_dev, surr_record *recs_out_dev,
+                                 void *stream);
+
+/* Records of the last surrogate_sweep before the final merge is converted:
+ * copies the k merged records (device) — used by the multi-GPU path to feed
+ * the allgather without a float->key round trip. */
+surr_status surrogate_sweep_records(surrogate_t *h, const surr_space *space, uint32_t k, surr_record *recs_dev,
+                                    void *stream);
+
+/* Decoder hook: digits of n consecutive indices starting at `first`, computed
+ * by the kernels' device decoder (super-digit magic division), written as
+ * uint8 digits_dev[n * P] (parameter 0 first). */
+surr_status surrogate_decode_range(surrogate_t *h, const surr_space *space, uint64_t first, uint64_t n,
+                                   uint8_t *digits_dev, void *stream);
+
+/* Exact |S| = prod r_j; SURR_E_RANGE if it does not fit u64. */
+surr_status surrogate_space_size(const surr_space *space, uint64_t *out);
+
+/* Timing of the fused sweep kernel alone (CUDA events recorded on the launch
+ * stream around every K1 launch while enabled).  get synchronises the events
+ * and returns the summed milliseconds and launch count since the last reset. */
+surr_status surrogate_kernel_timing(surrogate_t *h, int enable);
+surr_status surrogate_kernel_timing_get(surrogate_t *h, double *total_ms, uint32_t *launches);
+
+/* Number of kernel launches the last call issued on the GPU (for the bench's
+ * gpu_launches count). */
+uint32_t surrogate_last_launches(const surrogate_t *h);
+
+/* Self-test of one tcgen05 GEMM (test infrastructure for the UMMA encodings):
+ * D[128 x N] = A[128 x K] * B[K x N] with A staged in TMEM, B in shared memory
+ * (K-major, no swizzle), FP32 accumulate.  precision BF16 or TF32 (one pass).
+ * a_host / b_host / d_host are host float arrays (row-major). */
+surr_status surrogate_selftest_umma(int cuda_device, int precision, uint32_t n, uint32_t k, const float *a_host,
+                                    const float *b_host, float *d_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

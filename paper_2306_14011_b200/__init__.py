@@ -1,0 +1,283 @@
+"""B200-native exhaustive FCNN-surrogate sweep (arxiv 2306.14011 hot path).
+
+Thin ctypes binding over ``libsurrogate.so`` (C ABI in ``include/surrogate.h``):
+argument marshalling only — every step of the path (decode, normalisation,
+MLP layers, top-k, merges) runs in the CUDA kernels of ``csrc/``.  PyTorch is
+used for device memory and streams.  There is no CPU fallback: if the shared
+library is missing or the device is not sm_100 the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .build import LIB_PATH, build_library  # noqa: F401
+
+PREC = {"bf16": 0, "fp32": 1, "tf32": 2}
+K_MAX = 1024
+EXPORTS = [
+    "surrogate_create", "surrogate_destroy", "surrogate_last_error", "surrogate_load_weights",
+    "surrogate_predict", "surrogate_sweep", "surrogate_sweep_host", "surrogate_eval_range",
+    "surrogate_merge_topk", "surrogate_sweep_records", "surrogate_decode_range", "surrogate_space_size",
+    "surrogate_kernel_timing", "surrogate_kernel_timing_get", "surrogate_last_launches",
+    "surrogate_selftest_umma",
+]
+
+
+class SurrogateError(RuntimeError):
+    pass
+
+
+class _Space(ctypes.Structure):
+    _fields_ = [("num_params", ctypes.c_uint32), ("radix", ctypes.POINTER(ctypes.c_uint32)),
+                ("values", ctypes.POINTER(ctypes.c_double)), ("begin", ctypes.c_uint64),
+                ("end", ctypes.c_uint64)]
+
+
+class _Model(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_uint32), ("widths", ctypes.POINTER(ctypes.c_uint32)),
+                ("W", ctypes.POINTER(ctypes.POINTER(ctypes.c_double))),
+                ("b", ctypes.POINTER(ctypes.POINTER(ctypes.c_double))),
+                ("x_shift", ctypes.POINTER(ctypes.c_double)), ("x_scale", ctypes.POINTER(ctypes.c_double)),
+                ("y_mean", ctypes.c_double), ("y_scale", ctypes.c_double),
+                ("num_const_features", ctypes.c_uint32), ("const_features", ctypes.POINTER(ctypes.c_double)),
+                ("ensemble", ctypes.c_uint32), ("precision", ctypes.c_int)]
+
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree CUDA library; raise loudly when it is absent."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise SurrogateError(f"{LIB_PATH} not built (run __graft_entry__.build()); no CPU fallback exists")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
+        L.surrogate_create.argtypes = [i32, ctypes.POINTER(vp)]
+        L.surrogate_destroy.argtypes = [vp]
+        L.surrogate_destroy.restype = None
+        L.surrogate_last_error.argtypes = [vp]
+        L.surrogate_last_error.restype = ctypes.c_char_p
+        L.surrogate_load_weights.argtypes = [vp, ctypes.POINTER(_Model)]
+        L.surrogate_predict.argtypes = [vp, vp, u64, vp, vp]
+        L.surrogate_sweep.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp, ctypes.POINTER(u32), vp]
+        L.surrogate_sweep_host.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp, ctypes.POINTER(u32), vp]
+        L.surrogate_eval_range.argtypes = [vp, ctypes.POINTER(_Space), vp, vp]
+        L.surrogate_merge_topk.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
+        L.surrogate_sweep_records.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp]
+        L.surrogate_decode_range.argtypes = [vp, ctypes.POINTER(_Space), u64, u64, vp, vp]
+        L.surrogate_space_size.argtypes = [ctypes.POINTER(_Space), ctypes.POINTER(u64)]
+        L.surrogate_kernel_timing.argtypes = [vp, i32]
+        L.surrogate_kernel_timing_get.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u32)]
+        L.surrogate_last_launches.argtypes = [vp]
+        L.surrogate_last_launches.restype = u32
+        L.surrogate_selftest_umma.argtypes = [i32, i32, u32, u32, vp, vp, vp]
+        for name in EXPORTS:
+            fn = getattr(L, name)
+            if fn.restype is ctypes.c_int and name not in ("surrogate_last_launches",):
+                fn.restype = ctypes.c_int
+        _LIB = L
+    return _LIB
+
+
+def _ptr(a: np.ndarray, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def _check(rc: int, handle=None):
+    if rc != 0:
+        msg = lib().surrogate_last_error(handle).decode(errors="replace")
+        raise SurrogateError(f"status {rc}: {msg}")
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class SpaceDesc:
+    """Host-side search-space descriptor (value lists in Table order)."""
+
+    def __init__(self, value_lists, begin: int = 0, end: int = 0):
+        self.radix = np.ascontiguousarray([len(v) for v in value_lists], dtype=np.uint32)
+        self.values = np.ascontiguousarray(np.concatenate([np.asarray(v, np.float64) for v in value_lists]))
+        self.c = _Space(len(value_lists), _ptr(self.radix, ctypes.c_uint32), _ptr(self.values, ctypes.c_double),
+                        int(begin), int(end))
+
+
+def space_size(value_lists) -> int:
+    d = SpaceDesc(value_lists)
+    out = ctypes.c_uint64()
+    _check(lib().surrogate_space_size(ctypes.byref(d.c), ctypes.byref(out)))
+    return out.value
+
+
+class Surrogate:
+    """One handle on one CUDA device (surrogate_create / surrogate_destroy)."""
+
+    def __init__(self, device: int = 0):
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        _check(lib().surrogate_create(self.device, ctypes.byref(h)))
+        self.h = h
+        self.precision = None
+        self.P = None
+
+    def close(self):
+        if self.h:
+            lib().surrogate_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- model
+    def load(self, model: dict, precision: str = "bf16"):
+        """surrogate_load_weights from the model record of workloads.load_model."""
+        widths = np.ascontiguousarray(model["widths"], dtype=np.uint32)
+        members = model["members"]
+        L = len(widths) - 1
+        keep = []
+        Wp = (ctypes.POINTER(ctypes.c_double) * (L * len(members)))()
+        bp = (ctypes.POINTER(ctypes.c_double) * (L * len(members)))()
+        for e, m in enumerate(members):
+            for l in range(L):
+                w = np.ascontiguousarray(m["W"][l], dtype=np.float64)
+                b = np.ascontiguousarray(m["b"][l], dtype=np.float64)
+                keep += [w, b]
+                Wp[e * L + l] = _ptr(w, ctypes.c_double)
+                bp[e * L + l] = _ptr(b, ctypes.c_double)
+        xs = np.ascontiguousarray(model["x_shift"], dtype=np.float64)
+        xc = np.ascontiguousarray(model["x_scale"], dtype=np.float64)
+        cf = np.ascontiguousarray(model.get("const_features", np.zeros(0)), dtype=np.float64)
+        cfp = _ptr(cf, ctypes.c_double) if cf.size else ctypes.POINTER(ctypes.c_double)()
+        mc = _Model(L, _ptr(widths, ctypes.c_uint32), Wp, bp, _ptr(xs, ctypes.c_double),
+                    _ptr(xc, ctypes.c_double), float(model["y_mean"]), float(model["y_scale"]),
+                    int(cf.size), cfp, len(members), PREC[precision])
+        _check(lib().surrogate_load_weights(self.h, ctypes.byref(mc)), self.h)
+        self.precision = precision
+        self.P = int(widths[0]) - int(cf.size)
+        return self
+
+    # ---------------------------------------------------------------- calls
+    def sweep(self, value_lists, k: int, begin: int = 0, end: int = 0, stream=None):
+        """Top-k (idx int64 tensor, t float32 tensor, count) on the device."""
+        import torch
+        d = SpaceDesc(value_lists, begin, end)
+        idx = torch.empty(k, dtype=torch.int64, device=f"cuda:{self.device}")
+        t = torch.empty(k, dtype=torch.float32, device=f"cuda:{self.device}")
+        cnt = ctypes.c_uint32()
+        _check(lib().surrogate_sweep(self.h, ctypes.byref(d.c), k, ctypes.c_void_p(idx.data_ptr()),
+                                     ctypes.c_void_p(t.data_ptr()), ctypes.byref(cnt), _stream_ptr(stream)), self.h)
+        return idx, t, cnt.value
+
+    def sweep_into(self, desc: SpaceDesc, k: int, idx, t, stream=None) -> int:
+        """Allocation-free sweep into caller tensors (bench inner loop)."""
+        cnt = ctypes.c_uint32()
+        _check(lib().surrogate_sweep(self.h, ctypes.byref(desc.c), k, ctypes.c_void_p(idx.data_ptr()),
+                                     ctypes.c_void_p(t.data_ptr()), ctypes.byref(cnt), _stream_ptr(stream)), self.h)
+        return cnt.value
+
+    def sweep_host(self, value_lists, k: int, begin: int = 0, end: int = 0, stream=None, desc=None,
+                   out=None):
+        """End-to-end call with host outputs (numpy uint64 idx, float32 t, count)."""
+        d = desc if desc is not None else SpaceDesc(value_lists, begin, end)
+        if out is None:
+            out = (np.empty(k, np.uint64), np.empty(k, np.float32))
+        idx, t = out
+        cnt = ctypes.c_uint32()
+        _check(lib().surrogate_sweep_host(self.h, ctypes.byref(d.c), k, idx.ctypes.data_as(ctypes.c_void_p),
+                                          t.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt),
+                                          _stream_ptr(stream)), self.h)
+        return idx, t, cnt.value
+
+    def sweep_records(self, value_lists, k: int, begin: int = 0, end: int = 0, stream=None):
+        """Top-k as surr_record rows (int64 tensor [k, 2]: idx, key | pad << 32)."""
+        import torch
+        d = SpaceDesc(value_lists, begin, end)
+        recs = torch.empty((k, 2), dtype=torch.int64, device=f"cuda:{self.device}")
+        _check(lib().surrogate_sweep_records(self.h, ctypes.byref(d.c), k, ctypes.c_void_p(recs.data_ptr()),
+                                             _stream_ptr(stream)), self.h)
+        return recs
+
+    def merge_topk(self, recs, lists: int, k_in: int, k: int, stream=None):
+        """Merge `lists` sorted record lists (tensor [lists*k_in, 2]) into (idx, t, recs)."""
+        import torch
+        dev = f"cuda:{self.device}"
+        idx = torch.empty(k, dtype=torch.int64, device=dev)
+        t = torch.empty(k, dtype=torch.float32, device=dev)
+        out = torch.empty((k, 2), dtype=torch.int64, device=dev)
+        _check(lib().surrogate_merge_topk(self.h, ctypes.c_void_p(recs.data_ptr()), lists, k_in, k,
+                                          ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(t.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)), self.h)
+        return idx, t, out
+
+    def eval_range(self, value_lists, begin: int, end: int, stream=None):
+        """t(I) for every I in [begin, end) from the fused kernel (dense mode)."""
+        import torch
+        d = SpaceDesc(value_lists, begin, end)
+        t = torch.empty(end - begin, dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(lib().surrogate_eval_range(self.h, ctypes.byref(d.c), ctypes.c_void_p(t.data_ptr()),
+                                          _stream_ptr(stream)), self.h)
+        return t
+
+    def predict(self, x, stream=None):
+        """Explicit batch: x float32 [n, P] device tensor of raw values -> t [n]."""
+        import torch
+        x = x.contiguous()
+        if x.dtype != torch.float32 or x.dim() != 2 or x.shape[1] != self.P:
+            raise ValueError(f"x must be float32 [n, {self.P}]")
+        t = torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+        _check(lib().surrogate_predict(self.h, ctypes.c_void_p(x.data_ptr()), x.shape[0],
+                                       ctypes.c_void_p(t.data_ptr()), _stream_ptr(stream)), self.h)
+        return t
+
+    def decode_range(self, value_lists, first: int, n: int, stream=None):
+        import torch
+        d = SpaceDesc(value_lists)
+        out = torch.empty((n, len(value_lists)), dtype=torch.uint8, device=f"cuda:{self.device}")
+        _check(lib().surrogate_decode_range(self.h, ctypes.byref(d.c), first, n, ctypes.c_void_p(out.data_ptr()),
+                                            _stream_ptr(stream)), self.h)
+        return out
+
+    def kernel_timing(self, enable: bool):
+        _check(lib().surrogate_kernel_timing(self.h, 1 if enable else 0), self.h)
+
+    def kernel_timing_get(self):
+        ms = ctypes.c_double()
+        n = ctypes.c_uint32()
+        _check(lib().surrogate_kernel_timing_get(self.h, ctypes.byref(ms), ctypes.byref(n)), self.h)
+        return ms.value, n.value
+
+    def last_launches(self) -> int:
+        return int(lib().surrogate_last_launches(self.h))
+
+
+def selftest_umma(precision: str, A: np.ndarray, B: np.ndarray, device: int = 0) -> np.ndarray:
+    """D = A[128 x K] @ B[K x N] through one tcgen05 UMMA chain (test hook)."""
+    A = np.ascontiguousarray(A, np.float32)
+    B = np.ascontiguousarray(B, np.float32)
+    assert A.shape[0] == 128 and A.shape[1] == B.shape[0]
+    D = np.empty((128, B.shape[1]), np.float32)
+    rc = lib().surrogate_selftest_umma(device, PREC[precision], B.shape[1], A.shape[1],
+                                       A.ctypes.data_as(ctypes.c_void_p), B.ctypes.data_as(ctypes.c_void_p),
+                                       D.ctypes.data_as(ctypes.c_void_p))
+    _check(rc)
+    return D
+
+
+def key_to_float(keys: np.ndarray) -> np.ndarray:
+    """Inverse of the kernels' order-preserving float -> uint32 key (for records)."""
+    k = np.asarray(keys, np.uint32)
+    u = np.where(k & 0x80000000, k & 0x7FFFFFFF, ~k).astype(np.uint32)
+    return u.view(np.float32)

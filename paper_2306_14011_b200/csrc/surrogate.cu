@@ -1,0 +1,764 @@
+// Host runtime and C ABI of the B200 surrogate sweep (include/surrogate.h).
+//
+// Responsibilities: validate descriptors, compute |S| and
+// the decoder's super-digit magic numbers, build the value lookup table
+// (StandardScaler applied in double, then rounded to the
+// operand format), fold b_1 / device features / y de-standardisation into the
+// layer parameters, pack the UMMA shared-memory image, own device buffers and
+// launch K1 (sweep_kernel), K2 (merge_kernel) and K3 (sweep_kernel in predict
+// mode).  No arithmetic of the method runs here per config: every config is
+// evaluated by the kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sweep_kernel.cuh"
+
+using namespace surr;
+
+struct surrogate {
+  int dev = -1;
+  int sms = 0;
+  std::string err;
+  // model
+  bool loaded = false;
+  int prec = 0;
+  uint32_t H = 0, NL = 0, P = 0;
+  std::vector<uint8_t> wimg;
+  void* d_w = nullptr;
+  size_t d_w_cap = 0;
+  KParams mp{};  // model part of the kernel parameters
+  double* d_zshift = nullptr;
+  double* d_zscale = nullptr;
+  std::vector<double> hshift, hscale;  // host copies of the input affine map
+  // space cache
+  bool space_valid = false;
+  std::vector<uint32_t> c_radix;
+  std::vector<double> c_values;
+  std::vector<uint8_t> lut;
+  void* d_lut = nullptr;
+  size_t d_lut_cap = 0;
+  KParams sp{};  // space part (decoder) of the kernel parameters
+  uint64_t card = 0;
+  // buffers
+  surr_record* d_recs = nullptr;
+  size_t d_recs_cap = 0;
+  surr_record* d_merged = nullptr;
+  uint64_t* d_idx = nullptr;
+  float* d_t = nullptr;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  uint32_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+surr_status fail(surrogate* h, surr_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf; else g_err = buf;
+  return st;
+}
+
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) return fail(h, SURR_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------ rounding (host)
+uint32_t f32_bits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+float bits_f32(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+uint16_t bf16_rne(float f) {  // same as __float2bfloat16_rn for finite values
+  uint32_t u = f32_bits(f);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FC0;
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+uint32_t tf32_rna(float f) {  // same as cvt.rna.tf32.f32 for finite values
+  uint32_t u = f32_bits(f);
+  if ((u & 0x7FFFFFFFu) >= 0x7F800000u) return u;
+  return (u + 0x1000u) & 0xFFFFE000u;
+}
+void tf32_split(double x, uint32_t* hi, uint32_t* lo) {
+  float f = (float)x;
+  *hi = tf32_rna(f);
+  *lo = tf32_rna(f - bits_f32(*hi));
+}
+
+// K-major, no-swizzle UMMA operand image of an N x K matrix (element (n,k) =
+// B[k][n] of the fan_in x fan_out weight): core matrices 8 rows x 16 B,
+// K-adjacent core matrices 128 B apart (LBO), 8-row groups SBO apart.
+size_t pack_offset(uint32_t n, uint32_t k, uint32_t K, uint32_t esize) {
+  const uint32_t kc = 16 / esize;
+  const uint32_t sbo = (K / kc) * 128;
+  return (size_t)(n / 8) * sbo + (size_t)(k / kc) * 128 + (n % 8) * 16 + (k % kc) * esize;
+}
+
+uint32_t make_idesc(int fmt, uint32_t N, uint32_t M) {
+  // c_format F32 (bits 4-5 = 1), a/b format (bits 7-9, 10-12), K-major A and B,
+  // n_dim = N >> 3 (bits 17-22), m_dim = M >> 4 (bits 24-28)
+  return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool mul_ovf(uint64_t a, uint64_t b, uint64_t* out) { return __builtin_mul_overflow(a, b, out); }
+
+// ------------------------------------------------------------ kernel table
+struct KernelInfo {
+  const void* fn;
+  int nslot, threads;
+};
+
+template <int PREC, int H>
+KernelInfo kinfo() {
+  using C = Cfg<PREC, H>;
+  return KernelInfo{(const void*)&sweep_kernel<PREC, H>, C::NSLOT, C::THREADS};
+}
+
+bool get_kernel(int prec, uint32_t H, KernelInfo* ki) {
+#define CASE(P_, H_) \
+  if (prec == P_ && H == H_) { *ki = kinfo<P_, H_>(); return true; }
+  CASE(PREC_BF16, 32) CASE(PREC_BF16, 64) CASE(PREC_BF16, 128)
+  CASE(PREC_FP32, 32) CASE(PREC_FP32, 64) CASE(PREC_FP32, 128)
+  CASE(PREC_TF32, 32) CASE(PREC_TF32, 64) CASE(PREC_TF32, 128)
+#undef CASE
+  return false;
+}
+
+surr_status check_device(surrogate* h, int dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) return fail(h, SURR_E_NO_DEVICE, "no CUDA device");
+  if (dev < 0 || dev >= n) return fail(h, SURR_E_NO_DEVICE, "device %d out of range (%d devices)", dev, n);
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(h, SURR_E_NO_DEVICE, "device %d is sm_%d%d, this library is built for sm_100a", dev, prop.major,
+                prop.minor);
+  return SURR_OK;
+}
+
+// ------------------------------------------------------------ space / LUT
+surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
+  if (!sp || !sp->radix || !sp->values) return fail(h, SURR_E_INVALID_ARG, "null space descriptor");
+  const uint32_t P = sp->num_params;
+  if (P == 0 || P > SURR_MAX_PARAMS) return fail(h, SURR_E_INVALID_ARG, "num_params %u out of range", P);
+  if (P != h->P) return fail(h, SURR_E_INVALID_ARG, "space has %u params, model expects %u", P, h->P);
+  uint64_t card = 1, nvals = 0;
+  for (uint32_t j = 0; j < P; ++j) {
+    if (sp->radix[j] == 0) return fail(h, SURR_E_INVALID_ARG, "radix[%u] == 0", j);
+    if (mul_ovf(card, sp->radix[j], &card)) return fail(h, SURR_E_RANGE, "|S| does not fit in 64 bits");
+    nvals += sp->radix[j];
+  }
+  std::vector<uint32_t> radix(sp->radix, sp->radix + P);
+  std::vector<double> values(sp->values, sp->values + nvals);
+  for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j)
+    for (uint32_t d = 1; d < radix[j]; ++d)
+      if (!(values[o + d] > values[o + d - 1]))
+        return fail(h, SURR_E_INVALID_ARG, "value list %u not strictly increasing", j);
+  const uint64_t end = sp->end ? sp->end : card;
+  if (sp->begin > end || end > card)
+    return fail(h, SURR_E_INVALID_ARG, "bad range [%llu, %llu) of |S| = %llu", (unsigned long long)sp->begin,
+                (unsigned long long)end, (unsigned long long)card);
+  h->sp.begin = sp->begin;
+  h->sp.end = end;
+  h->card = card;
+  if (!force && h->space_valid && radix == h->c_radix && values == h->c_values) return SURR_OK;
+
+  // super digits: group g holds K slots 2g, 2g+1 (params, then the ones slot P)
+  const uint32_t G = (P + 1) / 2;
+  const bool bf = h->prec == PREC_BF16;
+  const size_t esz = bf ? 4 : 16;
+  std::vector<uint64_t> R(G);
+  std::vector<uint32_t> off(G);
+  size_t entries = 0;
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint32_t a = 2 * g, b = 2 * g + 1;
+    R[g] = (uint64_t)radix[a] * (b < P ? radix[b] : 1u);
+    off[g] = (uint32_t)entries;
+    entries += R[g];
+  }
+  if (entries * esz > 96 * 1024) return fail(h, SURR_E_UNSUPPORTED, "value table too large (%zu entries)", entries);
+  std::vector<uint32_t> voff(P);
+  for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
+  auto zval = [&](uint32_t j, uint32_t d) {  // StandardScaler / min-max affine map, double
+    return (values[voff[j] + d] - h->hshift[j]) / h->hscale[j];
+  };
+  std::vector<uint8_t> lut(align_up(entries * esz, 16), 0);
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint32_t a = 2 * g, b = 2 * g + 1;
+    const uint32_t rb = b < P ? radix[b] : 1u;
+    for (uint64_t D = 0; D < R[g]; ++D) {
+      const uint32_t da = (uint32_t)(D / rb), db = (uint32_t)(D % rb);
+      const double za = zval(a, da);
+      const double zb = b < P ? zval(b, db) : (b == P ? 1.0 : 0.0);
+      uint8_t* e = lut.data() + (off[g] + D) * esz;
+      if (bf) {
+        uint32_t w = (uint32_t)bf16_rne((float)za) | ((uint32_t)bf16_rne((float)zb) << 16);
+        memcpy(e, &w, 4);
+      } else {
+        uint32_t w[4];
+        tf32_split(za, &w[0], &w[2]);
+        tf32_split(zb, &w[1], &w[3]);
+        memcpy(e, w, 16);
+      }
+    }
+  }
+  // constant A0 columns after the groups (ones slot when P is even, zeros)
+  KParams& k = h->sp;
+  memset(k.a0_const, 0, sizeof k.a0_const);
+  for (uint32_t slot = 2 * G; slot < (uint32_t)K0; ++slot) {
+    const float v = slot == P ? 1.0f : 0.0f;
+    if (bf) {
+      uint32_t w = bf16_rne(v);
+      k.a0_const[slot / 2] |= (slot & 1) ? (w << 16) : w;
+    } else {
+      k.a0_const[slot] = tf32_rna(v);
+      k.a0_const[K0 + slot] = 0;
+    }
+  }
+  // decoder split: groups [split, G) from I mod M_lo (M_lo <= 2^31), the rest from I div M_lo
+  uint32_t split = G;
+  uint64_t mlo = 1;
+  while (split > 0 && mlo * R[split - 1] <= (1ull << 31)) { mlo *= R[split - 1]; --split; }
+  if (split == 0 && card + 4096 >= (1ull << 31)) {  // keep every decoded index below 2^31
+    split = 1;
+    mlo = 1;
+    for (uint32_t g = 1; g < G; ++g) mlo *= R[g];
+  }
+  if (split > 0) {
+    if (split == G) return fail(h, SURR_E_RANGE, "a single super digit exceeds 2^31");
+    if ((card / mlo) + 2 >= (1ull << 31)) return fail(h, SURR_E_RANGE, "|S| too large for the two-word decoder");
+  }
+  k.G = G;
+  k.split = split;
+  k.M_lo = split ? (uint32_t)mlo : 0x80000000u;
+  for (uint32_t g = 0; g < (uint32_t)MAXG; ++g) {
+    if (g < G) {
+      const uint64_t d = R[g];
+      uint32_t l = 0;
+      while ((1ull << l) < d) ++l;
+      const unsigned __int128 num = (unsigned __int128)1 << (31 + l);
+      const uint64_t m = (uint64_t)((num + d - 1) / d);
+      if (m > 0xFFFFFFFFull) return fail(h, SURR_E_RANGE, "magic number overflow");
+      k.R[g] = (uint32_t)d;
+      k.magic[g] = (uint32_t)m;
+      k.shft[g] = l;
+      k.lut_off[g] = off[g];
+    } else {
+      k.R[g] = 1; k.magic[g] = 0x80000000u; k.shft[g] = 0; k.lut_off[g] = 0;
+    }
+  }
+  if (lut.size() > h->d_lut_cap) {
+    if (h->d_lut) cudaFree(h->d_lut);
+    h->d_lut = nullptr;
+    if (cudaMalloc(&h->d_lut, lut.size()) != cudaSuccess) return fail(h, SURR_E_OOM, "cudaMalloc lut");
+    h->d_lut_cap = lut.size();
+  }
+  CU(cudaMemcpy(h->d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
+  k.lut_gmem = h->d_lut;
+  k.lut_bytes = (uint32_t)lut.size();
+  h->lut.swap(lut);
+  h->c_radix = radix;
+  h->c_values = values;
+  h->space_valid = true;
+  return SURR_OK;
+}
+
+struct Launch {
+  KernelInfo ki;
+  int grid;
+  size_t smem;
+  KParams p;
+};
+
+surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L) {
+  if (!get_kernel(h->prec, h->H, &L->ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
+  KParams p = h->mp;
+  const KParams& s = h->sp;
+  if (mode != MODE_PREDICT) {
+    p.G = s.G; p.split = s.split; p.M_lo = s.M_lo;
+    memcpy(p.R, s.R, sizeof p.R); memcpy(p.magic, s.magic, sizeof p.magic);
+    memcpy(p.shft, s.shft, sizeof p.shft); memcpy(p.lut_off, s.lut_off, sizeof p.lut_off);
+    memcpy(p.a0_const, s.a0_const, sizeof p.a0_const);
+    p.lut_gmem = s.lut_gmem; p.lut_bytes = s.lut_bytes;
+  } else {
+    p.G = 0; p.split = 0; p.M_lo = 0x80000000u; p.lut_bytes = 0;
+  }
+  p.begin = begin;
+  p.end = end;
+  p.num_tiles = (end - begin + TILE_M - 1) / TILE_M;
+  const int nslot = L->ki.nslot;
+  uint64_t want = (p.num_tiles + nslot - 1) / nslot;
+  L->grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms, want));
+  p.dTiles = (uint32_t)(nslot * L->grid);
+  const uint64_t delta = (uint64_t)p.dTiles * TILE_M;
+  if (p.split) { p.dhi = (uint32_t)(delta / p.M_lo); p.dlo = (uint32_t)(delta % p.M_lo); }
+  else { p.dhi = 0; p.dlo = (uint32_t)delta; }
+  p.k = mode == MODE_TOPK ? k : 1;
+  // dynamic shared memory layout
+  size_t off = align_up(p.w_bytes, 128);
+  p.smem_lut = (uint32_t)off;
+  off = align_up(off + (mode == MODE_PREDICT ? 0 : p.lut_bytes), 128);
+  p.smem_lists = (uint32_t)off;
+  off += (mode == MODE_TOPK ? 2ull * k * sizeof(surr_record) : 0);
+  off = align_up(off, 128);
+  p.smem_cand = (uint32_t)off;
+  off += (mode == MODE_TOPK ? (size_t)nslot * 4 * CAND_CAP * sizeof(surr_record) : 0);
+  off = align_up(off, 128);
+  p.smem_misc = (uint32_t)off;
+  off += 256;
+  L->smem = off;
+  if (L->smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "shared memory %zu B exceeds 227 KB", L->smem);
+  L->p = p;
+  return SURR_OK;
+}
+
+surr_status launch(surrogate* h, Launch& L, int mode, cudaStream_t st) {
+  CU(cudaFuncSetAttribute(L.ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing && mode == MODE_TOPK) {
+    if (h->ev_used + 2 > h->ev.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        h->ev.push_back(e);
+      }
+    }
+    e0 = h->ev[h->ev_used];
+    e1 = h->ev[h->ev_used + 1];
+    h->ev_used += 2;
+    CU(cudaEventRecord(e0, st));
+  }
+  void* args[] = {(void*)&L.p, (void*)&mode};
+  CU(cudaLaunchKernel(L.ki.fn, dim3(L.grid), dim3(L.ki.threads), args, L.smem, st));
+  if (e1) CU(cudaEventRecord(e1, st));
+  ++h->launches;
+  return SURR_OK;
+}
+
+surr_status ensure_recs(surrogate* h, size_t n) {
+  if (n <= h->d_recs_cap) return SURR_OK;
+  if (h->d_recs) cudaFree(h->d_recs);
+  h->d_recs = nullptr;
+  if (cudaMalloc(&h->d_recs, n * sizeof(surr_record)) != cudaSuccess) return fail(h, SURR_E_OOM, "cudaMalloc recs");
+  h->d_recs_cap = n;
+  return SURR_OK;
+}
+
+surr_status launch_merge(surrogate* h, const surr_record* in, uint32_t lists, uint32_t k_in, uint32_t k,
+                         uint64_t* oi, float* ot, surr_record* orec, cudaStream_t st) {
+  const size_t smem = (2ull * k + k_in) * sizeof(surr_record);
+  if (smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "merge needs %zu B shared memory", smem);
+  CU(cudaFuncSetAttribute((const void*)merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  uint32_t threads = std::min<uint32_t>(1024u, (std::max(k, k_in) + 31) / 32 * 32);
+  merge_kernel<<<1, threads, smem, st>>>(in, lists, k_in, k, oi, ot, orec);
+  CU(cudaGetLastError());
+  ++h->launches;
+  return SURR_OK;
+}
+
+surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint64_t* idx_dev, float* t_dev,
+                         surr_record* recs_dev, uint32_t* count_host, cudaStream_t st, bool force) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "no model loaded");
+  if (k == 0 || k > SURR_K_MAX) return fail(h, SURR_E_INVALID_ARG, "k = %u outside 1..%u", k, SURR_K_MAX);
+  CU(cudaSetDevice(h->dev));
+  surr_status rc = prepare_space(h, space, force);
+  if (rc) return rc;
+  const uint64_t begin = h->sp.begin, end = h->sp.end;
+  const uint64_t n = end - begin;
+  if (count_host) *count_host = (uint32_t)std::min<uint64_t>(k, n);
+  h->launches = 0;
+  if (n == 0) {
+    // empty range: all-sentinel result through the merge kernel (zero lists)
+    return launch_merge(h, h->d_recs, 0, k, k, idx_dev, t_dev, recs_dev, st);
+  }
+  Launch L;
+  rc = plan(h, begin, end, k, MODE_TOPK, &L);
+  if (rc) return rc;
+  rc = ensure_recs(h, (size_t)L.grid * k);
+  if (rc) return rc;
+  L.p.recs = h->d_recs;
+  rc = launch(h, L, MODE_TOPK, st);
+  if (rc) return rc;
+  return launch_merge(h, h->d_recs, (uint32_t)L.grid, k, k, idx_dev, t_dev, recs_dev, st);
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+surr_status surrogate_create(int cuda_device, surrogate_t** out) {
+  if (!out) return fail(nullptr, SURR_E_INVALID_ARG, "null out");
+  *out = nullptr;
+  surrogate* h = nullptr;
+  surr_status rc = check_device(nullptr, cuda_device);
+  if (rc) return rc;
+  h = new surrogate();
+  h->dev = cuda_device;
+  if (cudaSetDevice(cuda_device) != cudaSuccess) { delete h; return fail(nullptr, SURR_E_CUDA, "cudaSetDevice"); }
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (cudaMalloc(&h->d_merged, SURR_K_MAX * sizeof(surr_record)) != cudaSuccess) {
+    delete h;
+    return fail(nullptr, SURR_E_OOM, "cudaMalloc");
+  }
+  *out = h;
+  return SURR_OK;
+}
+
+void surrogate_destroy(surrogate_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  cudaFree(h->d_w); cudaFree(h->d_lut); cudaFree(h->d_recs); cudaFree(h->d_merged);
+  cudaFree(h->d_zshift); cudaFree(h->d_zscale);
+  for (auto e : h->ev) cudaEventDestroy(e);
+  delete h;
+}
+
+const char* surrogate_last_error(const surrogate_t* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+uint32_t surrogate_last_launches(const surrogate_t* h) { return h ? h->launches : 0; }
+
+surr_status surrogate_space_size(const surr_space* sp, uint64_t* out) {
+  surrogate* h = nullptr;
+  if (!sp || !out || !sp->radix) return fail(h, SURR_E_INVALID_ARG, "null argument");
+  if (sp->num_params == 0 || sp->num_params > SURR_MAX_PARAMS) return fail(h, SURR_E_INVALID_ARG, "num_params");
+  uint64_t c = 1;
+  for (uint32_t j = 0; j < sp->num_params; ++j) {
+    if (sp->radix[j] == 0) return fail(h, SURR_E_INVALID_ARG, "radix[%u] == 0", j);
+    if (mul_ovf(c, sp->radix[j], &c)) return fail(h, SURR_E_RANGE, "|S| does not fit in 64 bits");
+  }
+  *out = c;
+  return SURR_OK;
+}
+
+surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
+  if (!h || !m || !m->widths || !m->W || !m->b || !m->x_shift || !m->x_scale)
+    return fail(h, SURR_E_INVALID_ARG, "null argument");
+  const uint32_t L = m->num_layers;
+  if (L < 2 || L - 1 > SURR_MAX_HIDDEN_LAYERS)
+    return fail(h, SURR_E_UNSUPPORTED, "num_layers %u: need 1..%u hidden layers", L, SURR_MAX_HIDDEN_LAYERS);
+  if (m->ensemble != 1) return fail(h, SURR_E_UNSUPPORTED, "ensemble %u: only E == 1 in this build", m->ensemble);
+  if (m->precision != SURR_PREC_BF16 && m->precision != SURR_PREC_FP32 && m->precision != SURR_PREC_TF32)
+    return fail(h, SURR_E_INVALID_ARG, "precision %d", (int)m->precision);
+  const uint32_t F = m->widths[0], H = m->widths[1];
+  if (m->widths[L] != 1) return fail(h, SURR_E_INVALID_ARG, "output width must be 1");
+  for (uint32_t l = 1; l < L; ++l)
+    if (m->widths[l] != H) return fail(h, SURR_E_UNSUPPORTED, "hidden widths must be equal");
+  if (H != 32 && H != 64 && H != 128) return fail(h, SURR_E_UNSUPPORTED, "hidden width %u not in {32,64,128}", H);
+  if (m->num_const_features > F || (m->num_const_features && !m->const_features))
+    return fail(h, SURR_E_INVALID_ARG, "const features");
+  const uint32_t P = F - m->num_const_features;
+  if (P == 0 || P + 1 > (uint32_t)K0) return fail(h, SURR_E_UNSUPPORTED, "%u tuning parameters: need 1..15", P);
+  for (uint32_t l = 0; l < L; ++l)
+    if (!m->W[l] || !m->b[l]) return fail(h, SURR_E_INVALID_ARG, "null layer %u", l);
+  CU(cudaSetDevice(h->dev));
+
+  const int prec = m->precision == SURR_PREC_BF16 ? PREC_BF16 : m->precision == SURR_PREC_FP32 ? PREC_FP32 : PREC_TF32;
+  const uint32_t NL = L - 1;
+  std::vector<double> shift(F), scale(F);
+  for (uint32_t j = 0; j < F; ++j) {
+    shift[j] = m->x_shift[j];
+    scale[j] = m->x_scale[j] == 0.0 ? 1.0 : m->x_scale[j];
+  }
+  // layer 1 operand rows: z_0..z_{P-1}, ones slot carrying b_1 + W1[const] z_const, zeros
+  const double* W1 = m->W[0];
+  std::vector<double> B1((size_t)K0 * H, 0.0);  // [k][n]
+  for (uint32_t kk = 0; kk < P; ++kk)
+    for (uint32_t n = 0; n < H; ++n) B1[(size_t)kk * H + n] = W1[(size_t)kk * H + n];
+  for (uint32_t n = 0; n < H; ++n) {
+    double b = m->b[0][n];
+    for (uint32_t c = 0; c < m->num_const_features; ++c) {
+      const double zc = (m->const_features[c] - shift[P + c]) / scale[P + c];
+      b += W1[(size_t)(P + c) * H + n] * zc;
+    }
+    B1[(size_t)P * H + n] = b;
+  }
+  const bool bf = prec == PREC_BF16;
+  const uint32_t esz = bf ? 2 : 4;
+  const bool lo1 = !bf;                  // layer 1 carries a lo part in both TF32 modes
+  const bool loh = prec == PREC_FP32;    // hidden layers carry a lo part (3xTF32)
+  const size_t b1_bytes = (size_t)H * K0 * esz;
+  const size_t bh_bytes = (size_t)H * H * esz;
+  KParams& p = h->mp;
+  p = KParams{};
+  size_t off = 0;
+  p.off_b1 = (uint32_t)off; off += b1_bytes;
+  p.off_b1lo = lo1 ? (uint32_t)off : p.off_b1; off += lo1 ? b1_bytes : 0;
+  off = align_up(off, 128);
+  p.off_bh = (uint32_t)off;
+  p.lo_delta_h = (uint32_t)bh_bytes;
+  p.stride_bh = (uint32_t)align_up(bh_bytes * (loh ? 2 : 1), 128);
+  off += (size_t)(NL - 1) * p.stride_bh;
+  off = align_up(off, 128);
+  p.off_bias = (uint32_t)off; off += (size_t)std::max<uint32_t>(NL >= 2 ? NL - 2 : 0, 1) * H * 4;
+  off = align_up(off, 16);
+  p.off_nb = (uint32_t)off; off += H * 4;
+  p.off_w = (uint32_t)off; off += H * 4;
+  p.w_bytes = (uint32_t)align_up(off, 128);
+  std::vector<uint8_t> img(p.w_bytes, 0);
+
+  auto put = [&](size_t base, const double* src, uint32_t K, uint32_t N, bool lo_part, size_t lo_base) {
+    // src is [K][N] (fan_in x fan_out); operand element (n, k)
+    for (uint32_t kk = 0; kk < K; ++kk)
+      for (uint32_t n = 0; n < N; ++n) {
+        const double x = src[(size_t)kk * N + n];
+        const size_t o = pack_offset(n, kk, K, esz);
+        if (bf) {
+          uint16_t v = bf16_rne((float)x);
+          memcpy(&img[base + o], &v, 2);
+        } else {
+          uint32_t hi, lo;
+          tf32_split(x, &hi, &lo);
+          memcpy(&img[base + o], &hi, 4);
+          if (lo_part) memcpy(&img[lo_base + o], &lo, 4);
+        }
+      }
+  };
+  put(p.off_b1, B1.data(), K0, H, lo1, p.off_b1lo);
+  for (uint32_t l = 1; l < NL; ++l) {
+    const size_t base = p.off_bh + (size_t)(l - 1) * p.stride_bh;
+    put(base, m->W[l], H, H, loh, base + bh_bytes);
+  }
+  float* fb = reinterpret_cast<float*>(&img[p.off_bias]);
+  for (uint32_t l = 1; l + 1 < NL; ++l)  // biases of model layers 2 .. NL-1 (hidden epilogues)
+    for (uint32_t n = 0; n < H; ++n) fb[(size_t)(l - 1) * H + n] = (float)m->b[l][n];
+  // final layer: t = y_mean + y_scale (sum_j w_j relu(D_j + b_j) + b_out)
+  //            = c' + sum_j w'_j max(D_j, -b_j),  w' = y_scale w,  c' = y_mean + y_scale (b_out + sum w b)
+  const double* Wout = m->W[NL];
+  const double bout = m->b[NL][0];
+  const double* bl = NL >= 2 ? m->b[NL - 1] : nullptr;  // layer-1 bias is already in D when NL == 1
+  float* fnb = reinterpret_cast<float*>(&img[p.off_nb]);
+  float* fw = reinterpret_cast<float*>(&img[p.off_w]);
+  double cacc = bout;
+  for (uint32_t n = 0; n < H; ++n) {
+    const double bj = bl ? bl[n] : 0.0;
+    fnb[n] = (float)(-bj);
+    fw[n] = (float)(m->y_scale * Wout[n]);
+    cacc += Wout[n] * bj;
+  }
+  p.c_out = (float)(m->y_mean + m->y_scale * cacc);
+  p.NL = NL;
+  p.sbo_b1 = (K0 / (16 / esz)) * 128;
+  p.sbo_bh = (H / (16 / esz)) * 128;
+  const int fmt = bf ? 1 : 2;
+  p.idesc_l1 = make_idesc(fmt, H, TILE_M);
+  p.idesc_h = make_idesc(fmt, H, TILE_M);
+  p.P = P;
+
+  if (img.size() > h->d_w_cap) {
+    cudaFree(h->d_w);
+    h->d_w = nullptr;
+    if (cudaMalloc(&h->d_w, img.size()) != cudaSuccess) return fail(h, SURR_E_OOM, "cudaMalloc weights");
+    h->d_w_cap = img.size();
+  }
+  CU(cudaMemcpy(h->d_w, img.data(), img.size(), cudaMemcpyHostToDevice));
+  p.w_gmem = h->d_w;
+  if (!h->d_zshift) {
+    if (cudaMalloc(&h->d_zshift, 32 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&h->d_zscale, 32 * sizeof(double)) != cudaSuccess)
+      return fail(h, SURR_E_OOM, "cudaMalloc");
+  }
+  CU(cudaMemcpy(h->d_zshift, shift.data(), P * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(h->d_zscale, scale.data(), P * sizeof(double), cudaMemcpyHostToDevice));
+  p.zshift = h->d_zshift;
+  p.zscale = h->d_zscale;
+  h->hshift = shift;
+  h->hscale = scale;
+  h->wimg.swap(img);
+  h->prec = prec;
+  h->H = H;
+  h->NL = NL;
+  h->P = P;
+  h->loaded = true;
+  h->space_valid = false;
+  h->c_values.clear();
+  h->c_radix.clear();
+  return SURR_OK;
+}
+
+surr_status surrogate_sweep(surrogate_t* h, const surr_space* space, uint32_t k, uint64_t* idx_dev, float* t_dev,
+                            uint32_t* count_host, void* stream) {
+  if (h && (!idx_dev || !t_dev)) return fail(h, SURR_E_INVALID_ARG, "null output");
+  return sweep_common(h, space, k, idx_dev, t_dev, nullptr, count_host, (cudaStream_t)stream, false);
+}
+
+surr_status surrogate_sweep_records(surrogate_t* h, const surr_space* space, uint32_t k, surr_record* recs_dev,
+                                    void* stream) {
+  if (h && !recs_dev) return fail(h, SURR_E_INVALID_ARG, "null output");
+  return sweep_common(h, space, k, nullptr, nullptr, recs_dev, nullptr, (cudaStream_t)stream, false);
+}
+
+surr_status surrogate_sweep_host(surrogate_t* h, const surr_space* space, uint32_t k, uint64_t* idx_host,
+                                 float* t_host, uint32_t* count_host, void* stream) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  if (!idx_host || !t_host) return fail(h, SURR_E_INVALID_ARG, "null output");
+  if (k == 0 || k > SURR_K_MAX) return fail(h, SURR_E_INVALID_ARG, "k = %u outside 1..%u", k, SURR_K_MAX);
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaSetDevice(h->dev));
+  if (!h->d_idx) {
+    if (cudaMalloc(&h->d_idx, SURR_K_MAX * 8) != cudaSuccess || cudaMalloc(&h->d_t, SURR_K_MAX * 4) != cudaSuccess)
+      return fail(h, SURR_E_OOM, "cudaMalloc");
+  }
+  surr_status rc = sweep_common(h, space, k, h->d_idx, h->d_t, nullptr, count_host, st, true);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(idx_host, h->d_idx, (size_t)k * 8, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(t_host, h->d_t, (size_t)k * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return SURR_OK;
+}
+
+surr_status surrogate_eval_range(surrogate_t* h, const surr_space* space, float* t_dev, void* stream) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "no model loaded");
+  if (!t_dev) return fail(h, SURR_E_INVALID_ARG, "null output");
+  CU(cudaSetDevice(h->dev));
+  surr_status rc = prepare_space(h, space, false);
+  if (rc) return rc;
+  h->launches = 0;
+  if (h->sp.end == h->sp.begin) return SURR_OK;
+  Launch L;
+  rc = plan(h, h->sp.begin, h->sp.end, 1, MODE_DENSE, &L);
+  if (rc) return rc;
+  L.p.t_dense = t_dev;
+  return launch(h, L, MODE_DENSE, (cudaStream_t)stream);
+}
+
+surr_status surrogate_predict(surrogate_t* h, const float* x_dev, uint64_t n, float* t_dev, void* stream) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "no model loaded");
+  h->launches = 0;
+  if (n == 0) return SURR_OK;
+  if (!x_dev || !t_dev) return fail(h, SURR_E_INVALID_ARG, "null buffer");
+  CU(cudaSetDevice(h->dev));
+  Launch L;
+  surr_status rc = plan(h, 0, n, 1, MODE_PREDICT, &L);
+  if (rc) return rc;
+  L.p.x = x_dev;
+  L.p.t_dense = t_dev;
+  return launch(h, L, MODE_PREDICT, (cudaStream_t)stream);
+}
+
+surr_status surrogate_merge_topk(surrogate_t* h, const surr_record* recs_dev, uint32_t lists, uint32_t k_in,
+                                 uint32_t k, uint64_t* idx_dev, float* t_dev, surr_record* recs_out_dev,
+                                 void* stream) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  if (k == 0 || k > SURR_K_MAX || k_in == 0 || k_in > SURR_K_MAX)
+    return fail(h, SURR_E_INVALID_ARG, "k / k_in outside 1..%u", SURR_K_MAX);
+  if ((lists && !recs_dev) || (!idx_dev && !t_dev && !recs_out_dev)) return fail(h, SURR_E_INVALID_ARG, "null buffer");
+  CU(cudaSetDevice(h->dev));
+  h->launches = 0;
+  return launch_merge(h, recs_dev, lists, k_in, k, idx_dev, t_dev, recs_out_dev, (cudaStream_t)stream);
+}
+
+surr_status surrogate_decode_range(surrogate_t* h, const surr_space* space, uint64_t first, uint64_t n,
+                                   uint8_t* digits_dev, void* stream) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "load a model first (the table format follows its precision)");
+  if (n && !digits_dev) return fail(h, SURR_E_INVALID_ARG, "null output");
+  CU(cudaSetDevice(h->dev));
+  surr_status rc = prepare_space(h, space, false);
+  if (rc) return rc;
+  if (first > h->card || n > h->card - first) return fail(h, SURR_E_INVALID_ARG, "range outside |S|");
+  h->launches = 0;
+  if (n == 0) return SURR_OK;
+  DecodeParams dp{};
+  const KParams& s = h->sp;
+  dp.G = s.G; dp.split = s.split; dp.M_lo = s.M_lo; dp.P = h->P;
+  memcpy(dp.R, s.R, sizeof dp.R); memcpy(dp.magic, s.magic, sizeof dp.magic); memcpy(dp.shft, s.shft, sizeof dp.shft);
+  for (uint32_t j = 0; j < h->P; ++j) dp.radix[j] = h->c_radix[j];
+  dp.first = first; dp.n = n; dp.out = digits_dev;
+  const uint32_t threads = 256;
+  const uint64_t blocks = std::min<uint64_t>((n + threads - 1) / threads, 1u << 20);
+  decode_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(dp);
+  CU(cudaGetLastError());
+  ++h->launches;
+  return SURR_OK;
+}
+
+surr_status surrogate_kernel_timing(surrogate_t* h, int enable) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  h->timing = enable != 0;
+  h->ev_used = 0;
+  return SURR_OK;
+}
+
+surr_status surrogate_kernel_timing_get(surrogate_t* h, double* total_ms, uint32_t* launches) {
+  if (!h || !total_ms || !launches) return fail(h, SURR_E_INVALID_ARG, "null argument");
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+    CU(cudaEventSynchronize(h->ev[i + 1]));
+    float ms = 0.0f;
+    CU(cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+    tot += ms;
+  }
+  *total_ms = tot;
+  *launches = (uint32_t)(h->ev_used / 2);
+  return SURR_OK;
+}
+
+surr_status surrogate_selftest_umma(int cuda_device, int precision, uint32_t n, uint32_t k, const float* a_host,
+                                    const float* b_host, float* d_host) {
+  surrogate* h = nullptr;
+  if (!a_host || !b_host || !d_host) return fail(h, SURR_E_INVALID_ARG, "null argument");
+  const bool bf = precision == SURR_PREC_BF16;
+  if (!bf && precision != SURR_PREC_TF32) return fail(h, SURR_E_INVALID_ARG, "precision must be BF16 or TF32");
+  const uint32_t kstep = bf ? 16 : 8;
+  if (n < 32 || n > 256 || n % 32 || k == 0 || k % kstep || k > 256)
+    return fail(h, SURR_E_UNSUPPORTED, "selftest shape N=%u K=%u", n, k);
+  surr_status rc = check_device(h, cuda_device);
+  if (rc) return rc;
+  CU(cudaSetDevice(cuda_device));
+  const uint32_t esz = bf ? 2 : 4;
+  std::vector<uint8_t> img((size_t)n * k * esz, 0);
+  for (uint32_t kk = 0; kk < k; ++kk)
+    for (uint32_t j = 0; j < n; ++j) {
+      const float x = b_host[(size_t)kk * n + j];
+      const size_t o = pack_offset(j, kk, k, esz);
+      if (bf) { uint16_t v = bf16_rne(x); memcpy(&img[o], &v, 2); }
+      else { uint32_t v = tf32_rna(x); memcpy(&img[o], &v, 4); }
+    }
+  std::vector<uint32_t> a((size_t)128 * k, 0);  // TMEM image per row: bf16 pairs or tf32 words
+  for (uint32_t r = 0; r < 128; ++r)
+    for (uint32_t kk = 0; kk < k; ++kk) {
+      const float x = a_host[(size_t)r * k + kk];
+      if (bf) a[(size_t)r * k + kk / 2] |= (uint32_t)bf16_rne(x) << ((kk & 1) * 16);
+      else a[(size_t)r * k + kk] = tf32_rna(x);
+    }
+  void *dA = nullptr, *dB = nullptr, *dD = nullptr;
+  CU(cudaMalloc(&dA, a.size() * 4));
+  CU(cudaMalloc(&dB, img.size()));
+  CU(cudaMalloc(&dD, (size_t)128 * n * 4));
+  CU(cudaMemcpy(dA, a.data(), a.size() * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(dB, img.data(), img.size(), cudaMemcpyHostToDevice));
+  const uint32_t acols = bf ? k / 2 : k;
+  const uint32_t idesc = make_idesc(bf ? 1 : 2, n, TILE_M);
+  const uint32_t sbo = (k / (16 / esz)) * 128;
+  const size_t smem = align_up(img.size(), 128) + 64;
+  CU(cudaFuncSetAttribute((const void*)umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  umma_selftest_kernel<<<1, 128, smem>>>((const uint32_t*)dA, k, acols, (const uint8_t*)dB, (uint32_t)img.size(),
+                                          (float*)dD, n, bf ? 1 : 0, idesc, sbo);
+  CU(cudaGetLastError());
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(d_host, dD, (size_t)128 * n * 4, cudaMemcpyDeviceToHost));
+  cudaFree(dA); cudaFree(dB); cudaFree(dD);
+  return SURR_OK;
+}
+
+}  // extern "C"

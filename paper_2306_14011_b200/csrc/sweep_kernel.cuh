@@ -1,0 +1,654 @@
+// Fused exhaustive-sweep kernel (K1), explicit-batch predict (K3), block
+// top-k (a8) and the list merge (K2) for sm_100a.
+//
+// Per flat config index I:
+//   a2  mixed-radix decode, in registers, on "super digits" (pairs of
+//       parameters, radix R_g = r_{2g} r_{2g+1}) by 32-bit magic division;
+//   a3  normalisation prologue = one shared-memory lookup per super digit of
+//       the pre-normalised, pre-rounded operand pair;
+//   a4  layer-1 UMMA, K0 = 16 (14 params + ones column carrying b_1 + 0);
+//   a5  hidden epilogue: tcgen05.ld D -> (+b) -> ReLU -> BF16x2 / TF32 hi-lo
+//       -> tcgen05.st A (the next layer's A operand lives in TMEM);
+//   a6  hidden UMMAs, B = weights resident in shared memory (bulk-copied once);
+//   a7  final H -> 1 layer in FP32 on CUDA cores + de-standardisation;
+//   a8  warp ballot filter against the CTA's k-th best, per-warp candidate
+//       buffer, rank-based merge into the CTA's sorted top-k.
+//
+// CTA roles: warp 0 lane 0 issues every tcgen05.mma (work-conserving: it polls
+// the per-slot "A ready" mbarriers); warpgroups 1..NSLOT each own one TMEM
+// slot (D accumulator + A operand for a 128-row tile) and run decode,
+// epilogues and top-k for that slot's tiles, so NSLOT tiles are in flight and
+// one slot's CUDA-core epilogue overlaps the other slot's MMAs.
+#pragma once
+#include <cstdint>
+
+#include "sm100_ptx.cuh"
+#include "../../include/surrogate.h"
+
+namespace surr {
+
+enum { PREC_BF16 = 0, PREC_FP32 = 1, PREC_TF32 = 2 };
+enum { MODE_TOPK = 0, MODE_DENSE = 1, MODE_PREDICT = 2 };
+
+constexpr int MAXG = 8;       // super-digit groups (P <= 15 -> ceil(P/2) <= 8)
+constexpr int K0 = 16;        // layer-1 K (P + ones column <= 16)
+constexpr int TILE_M = 128;   // rows per tile (UMMA M)
+constexpr int CAND_CAP = 64;  // per-warp top-k candidate buffer
+constexpr uint32_t KEY_SENT = 0xFFFFFFFFu;
+constexpr uint64_t IDX_SENT = ~0ull;
+
+struct KParams {
+  // rows
+  uint64_t begin, end, num_tiles;
+  uint32_t dTiles;          // tile stride of one slot (= NSLOT * gridDim.x)
+  uint32_t dlo, dhi;        // dTiles * 128 split as dhi * M_lo + dlo
+  // decoder (super digits)
+  uint32_t G, split, M_lo;  // groups [split, G) decode from I mod M_lo, [0, split) from I div M_lo
+  uint32_t R[MAXG], magic[MAXG], shft[MAXG], lut_off[MAXG];
+  uint32_t a0_const[2 * K0];  // constant A0 columns past the LUT groups (bf16: [0, 8); tf32: hi [0,16), lo [16,32))
+  const void* lut_gmem;
+  uint32_t lut_bytes;
+  // predict rows
+  const float* x;
+  uint32_t P;
+  const double* zshift;     // [P]
+  const double* zscale;     // [P]
+  // model
+  uint32_t NL;              // UMMA layers (= number of hidden layers)
+  const void* w_gmem;
+  uint32_t w_bytes;
+  uint32_t off_b1, off_b1lo, off_bh, stride_bh, lo_delta_h, off_bias, off_nb, off_w;
+  uint32_t sbo_b1, sbo_bh;
+  uint32_t idesc_l1, idesc_h;
+  float c_out;
+  // outputs
+  uint32_t k;
+  surr_record* recs;        // MODE_TOPK: gridDim.x * k records
+  float* t_dense;           // MODE_DENSE / MODE_PREDICT
+  uint32_t smem_lut, smem_lists, smem_cand, smem_misc;  // byte offsets in dynamic smem
+};
+
+template <int PREC, int H>
+struct Cfg {
+  static constexpr int A_COLS = PREC == PREC_BF16 ? H / 2 : (PREC == PREC_FP32 ? 2 * H : H);
+  static constexpr int SLOT_COLS = H + A_COLS;
+  static constexpr int NSLOT = (2 * SLOT_COLS <= 512) ? 2 : 1;
+  static constexpr int NEED = NSLOT * SLOT_COLS;
+  static constexpr int TMEM_COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr int THREADS = 128 * (1 + NSLOT);
+  static constexpr int PASSES_H = PREC == PREC_FP32 ? 3 : 1;   // hidden layers
+  static constexpr int PASSES_1 = PREC == PREC_BF16 ? 1 : 3;   // layer 1
+  // A0 lo-part column offset (tf32 modes): fp32 keeps lo next to the hidden lo region
+  static constexpr int A0_LO = PREC == PREC_FP32 ? H : K0;
+  static_assert(SLOT_COLS * NSLOT <= 512, "TMEM budget");
+};
+
+// order-preserving float -> uint32 (NaN after +inf)
+__device__ __forceinline__ uint32_t f2key(float t) {
+  uint32_t u = __float_as_uint(t);
+  if (t != t) return KEY_SENT;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ bool rec_less(uint32_t ka, uint64_t ia, uint32_t kb, uint64_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+// SMEM matrix descriptor, K-major, SWIZZLE_NONE: core matrices of 8 rows x 16 B;
+// LBO = byte distance of K-adjacent core matrices (128), SBO = distance of
+// 8-row groups; version 1 (bits 46-47), layout type 0 (bits 61-63).
+__device__ __forceinline__ uint64_t make_bdesc(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((128u >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+
+// q = floor(n / d) for n < 2^31 with m = ceil(2^(31+l) / d), l = ceil(log2 d):
+// floor(2n * m / 2^32) >> l  (exact: m d - 2^(31+l) <= 2^l).
+__device__ __forceinline__ uint32_t magic_div(uint32_t n, uint32_t m, uint32_t l) {
+  return __umulhi(n + n, m) >> l;
+}
+
+// a2: super digits D_g of I = hi * M_lo + lo (groups [split, G) from lo, the
+// rest from hi), least significant group last; D_0 is clamped so that masked
+// rows past |S| still index inside the table.
+template <class PT>
+__device__ __forceinline__ void decode_groups(const PT& p, uint32_t lo, uint32_t hi, uint32_t (&D)[MAXG]) {
+#pragma unroll
+  for (int g = MAXG - 1; g >= 0; --g) {
+    D[g] = 0;
+    if (g < (int)p.G) {
+      const bool fromlo = g >= (int)p.split;
+      const uint32_t n = fromlo ? lo : hi;
+      const uint32_t q = magic_div(n, p.magic[g], p.shft[g]);
+      uint32_t dg = n - q * p.R[g];
+      if (g == 0) dg = min(dg, p.R[0] - 1u);
+      if (fromlo) lo = q; else hi = q;
+      D[g] = dg;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- top-k
+struct TopkShared {
+  surr_record* lists;  // [2][k]
+  surr_record* cand;   // [num epilogue warps][CAND_CAP]
+  volatile uint32_t* misc;  // [0] lock, [1] cur, [2] thr_key, [3..4] thr_idx
+};
+
+__device__ __forceinline__ uint32_t lower_bound_recs(const surr_record* a, uint32_t n, uint32_t key, uint64_t idx) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    surr_record r = a[mid];
+    if (rec_less(r.key, r.idx, key, idx)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Merge the warp's cnt candidates into the CTA list (caller holds the lock).
+__device__ void warp_merge(TopkShared& ts, surr_record* cand, uint32_t cnt, uint32_t k, uint32_t lane) {
+  // 1. sort candidates by rank (all keys distinct: idx unique)
+  surr_record c0, c1;
+  uint32_t r0 = 0, r1 = 0;
+  bool h0 = lane < cnt, h1 = lane + 32 < cnt;
+  if (h0) c0 = cand[lane];
+  if (h1) c1 = cand[lane + 32];
+  for (uint32_t j = 0; j < cnt; ++j) {
+    surr_record o = cand[j];
+    if (h0 && rec_less(o.key, o.idx, c0.key, c0.idx)) ++r0;
+    if (h1 && rec_less(o.key, o.idx, c1.key, c1.idx)) ++r1;
+  }
+  __syncwarp();
+  if (h0) cand[r0] = c0;
+  if (h1) cand[r1] = c1;
+  __syncwarp();
+  // 2. rank merge with the sorted list, keep the first k
+  uint32_t cur = ts.misc[1];
+  surr_record* L = ts.lists + (size_t)cur * k;
+  surr_record* O = ts.lists + (size_t)(cur ^ 1u) * k;
+  for (uint32_t i = lane; i < k; i += 32) {
+    surr_record e = L[i];
+    uint32_t p = i + lower_bound_recs(cand, cnt, e.key, e.idx);
+    if (p < k) O[p] = e;
+  }
+  for (uint32_t j = lane; j < cnt; j += 32) {
+    surr_record c = cand[j];
+    uint32_t p = j + lower_bound_recs(L, k, c.key, c.idx);
+    if (p < k) O[p] = c;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    surr_record last = O[k - 1];
+    ts.misc[1] = cur ^ 1u;
+    ts.misc[3] = (uint32_t)last.idx;
+    ts.misc[4] = (uint32_t)(last.idx >> 32);
+    ts.misc[2] = last.key;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void lock_acquire(TopkShared& ts, uint32_t lane) {
+  if (lane == 0) {
+    while (atomicCAS((uint32_t*)&ts.misc[0], 0u, 1u) != 0u) __nanosleep(32);
+    __threadfence_block();
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void lock_release(TopkShared& ts, uint32_t lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_block();
+    atomicExch((uint32_t*)&ts.misc[0], 0u);
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+template <int PREC, int H>
+__global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
+    sweep_kernel(const __grid_constant__ KParams p, int mode) {
+  using C = Cfg<PREC, H>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t lane = lane_id();
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_misc);  // [0] load, [1..2] a, [3..4] d
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.smem_misc + 64);
+  TopkShared ts;
+  ts.lists = reinterpret_cast<surr_record*>(smem + p.smem_lists);
+  ts.cand = reinterpret_cast<surr_record*>(smem + p.smem_cand);
+  ts.misc = reinterpret_cast<volatile uint32_t*>(smem + p.smem_misc + 128);
+
+  // ---- setup
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&bars[0], 1);
+      for (int s = 0; s < C::NSLOT; ++s) {
+        mbar_init(&bars[1 + s], 4);  // one arrive per epilogue warp
+        mbar_init(&bars[3 + s], 1);  // tcgen05.commit
+      }
+      fence_mbar_init();
+      fence_proxy_async_smem();
+      // weights (+ LUT) -> smem through the bulk-copy engine, one mbarrier
+      uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
+      mbar_arrive_expect_tx(&bars[0], total);
+      for (uint32_t off = 0; off < p.w_bytes; off += 32768u) {
+        uint32_t n = min(32768u, p.w_bytes - off);
+        bulk_g2s(smem + off, (const uint8_t*)p.w_gmem + off, n, &bars[0]);
+      }
+      if (mode != MODE_PREDICT && p.lut_bytes)
+        bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[0]);
+    }
+    __syncwarp();
+    tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  } else if (warp == 1 && mode == MODE_TOPK) {
+    for (uint32_t i = lane; i < p.k; i += 32) {
+      ts.lists[i].idx = IDX_SENT;
+      ts.lists[i].key = KEY_SENT;
+      ts.lists[i].pad = 0;
+    }
+    if (lane == 0) {
+      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= UMMA issuer (one thread) =================
+    if (lane == 0) {
+      mbar_wait(&bars[0], 0);  // weights resident
+      uint32_t left[C::NSLOT], layer[C::NSLOT], ph[C::NSLOT];
+      uint32_t active = 0;
+      for (int s = 0; s < C::NSLOT; ++s) {
+        uint64_t t0 = (uint64_t)blockIdx.x * C::NSLOT + s;
+        left[s] = t0 < p.num_tiles ? (uint32_t)((p.num_tiles - t0 - 1) / p.dTiles + 1) : 0u;
+        layer[s] = 0;
+        ph[s] = 0;
+        active += left[s] ? 1u : 0u;
+      }
+      const uint32_t sb = smem_u32(smem);
+      while (active) {
+#pragma unroll
+        for (int s = 0; s < C::NSLOT; ++s) {
+          if (!left[s] || !mbar_test(&bars[1 + s], ph[s])) continue;
+          ph[s] ^= 1u;
+          tc_fence_after();
+          const uint32_t d = tmem_base + s * C::SLOT_COLS;
+          const uint32_t a = d + H;
+          const uint32_t l = layer[s];
+          uint32_t bhi, blo, sbo, idesc, steps, passes, alo;
+          if (l == 0) {
+            bhi = sb + p.off_b1; blo = sb + p.off_b1lo; sbo = p.sbo_b1; idesc = p.idesc_l1;
+            steps = PREC == PREC_BF16 ? K0 / 16 : K0 / 8; passes = C::PASSES_1; alo = a + C::A0_LO;
+          } else {
+            bhi = sb + p.off_bh + (l - 1) * p.stride_bh; blo = bhi + p.lo_delta_h; sbo = p.sbo_bh;
+            idesc = p.idesc_h; steps = PREC == PREC_BF16 ? H / 16 : H / 8; passes = C::PASSES_H; alo = a + H;
+          }
+          for (uint32_t kk = 0; kk < steps; ++kk) {
+            const uint64_t dh = make_bdesc(bhi + kk * 256u, sbo);
+            if (PREC == PREC_BF16) {
+              umma_f16_ts(d, a + kk * 8u, dh, idesc, kk > 0);
+            } else {
+              umma_tf32_ts(d, a + kk * 8u, dh, idesc, kk > 0);
+              if (passes == 3) {
+                umma_tf32_ts(d, a + kk * 8u, make_bdesc(blo + kk * 256u, sbo), idesc, 1u);
+                umma_tf32_ts(d, alo + kk * 8u, dh, idesc, 1u);
+              }
+            }
+          }
+          umma_commit(&bars[3 + s]);
+          if (++layer[s] == p.NL) {
+            layer[s] = 0;
+            if (--left[s] == 0) --active;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= slot warpgroups: rows, epilogues, top-k =================
+    const uint32_t s = (warp >> 2) - 1;
+    const uint32_t wq = warp & 3u;
+    const uint32_t row = wq * 32u + lane;
+    const uint32_t tl = (wq * 32u) << 16;  // TMEM lane offset of this warp
+    const uint32_t dcol = tmem_base + tl + s * C::SLOT_COLS;
+    const uint32_t acol = dcol + H;
+    const float* sbias = reinterpret_cast<const float*>(smem + p.off_bias);
+    const float* snb = reinterpret_cast<const float*>(smem + p.off_nb);
+    const float* sw = reinterpret_cast<const float*>(smem + p.off_w);
+    const uint8_t* slut = smem + p.smem_lut;
+    surr_record* mycand = ts.cand + (size_t)(warp - 4) * CAND_CAP;
+    uint32_t ncand = 0;
+
+    uint64_t tile = (uint64_t)blockIdx.x * C::NSLOT + s;
+    uint64_t I = p.begin + tile * TILE_M + row;
+    uint32_t ilo, ihi;
+    if (p.split) { ihi = (uint32_t)(I / p.M_lo); ilo = (uint32_t)(I % p.M_lo); }
+    else { ihi = 0; ilo = (uint32_t)I; }
+    uint32_t phd = 0;
+    mbar_wait(&bars[0], 0);  // LUT / weights resident
+
+    for (; tile < p.num_tiles; tile += p.dTiles) {
+      const bool valid = I < p.end;
+      // ---------------- a2 + a3: A0 operand
+      uint32_t hi16[K0], lo16[K0];  // tf32: hi/lo slots; bf16: hi16[0..7] = packed columns
+      if (mode == MODE_PREDICT) {
+        // z_j = (x_j - shift_j) / scale_j in double (identical to the host LUT), slot P = 1
+        const uint64_t r = valid ? I : p.begin;
+        const float* xr = p.x + r * p.P;
+        float z[K0];
+#pragma unroll
+        for (int j = 0; j < K0; ++j) {
+          z[j] = 0.0f;
+          if (j < (int)p.P) z[j] = __double2float_rn(((double)xr[j] - p.zshift[j]) / p.zscale[j]);
+          else if (j == (int)p.P) z[j] = 1.0f;
+        }
+        if (PREC == PREC_BF16) {
+#pragma unroll
+          for (int c = 0; c < K0 / 2; ++c)
+            hi16[c] = bf16x2(z[2 * c], z[2 * c + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < K0; ++j) {
+            hi16[j] = to_tf32(z[j]);
+            lo16[j] = to_tf32(z[j] - __uint_as_float(hi16[j]));
+          }
+        }
+      } else {
+        uint32_t D[MAXG];
+        decode_groups(p, ilo, ihi, D);
+#pragma unroll
+        for (int g = 0; g < MAXG; ++g) {
+          if (g < (int)p.G) {
+            if (PREC == PREC_BF16) {
+              hi16[g] = reinterpret_cast<const uint32_t*>(slut)[p.lut_off[g] + D[g]];
+            } else {
+              const uint4 e = reinterpret_cast<const uint4*>(slut)[p.lut_off[g] + D[g]];
+              hi16[2 * g] = e.x; hi16[2 * g + 1] = e.y; lo16[2 * g] = e.z; lo16[2 * g + 1] = e.w;
+            }
+          } else {
+            if (PREC == PREC_BF16) {
+              hi16[g] = p.a0_const[g];
+            } else {
+              hi16[2 * g] = p.a0_const[2 * g]; hi16[2 * g + 1] = p.a0_const[2 * g + 1];
+              lo16[2 * g] = p.a0_const[K0 + 2 * g]; lo16[2 * g + 1] = p.a0_const[K0 + 2 * g + 1];
+            }
+          }
+        }
+      }
+      if (PREC == PREC_BF16) {
+        tmem_st8(acol, hi16);
+      } else {
+        tmem_st16(acol, hi16);
+        tmem_st16(acol + C::A0_LO, lo16);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[1 + s]);
+
+      // ---------------- layers
+      float t = 0.0f;
+      for (uint32_t l = 0; l < p.NL; ++l) {
+        mbar_wait(&bars[3 + s], phd);
+        phd ^= 1u;
+        tc_fence_after();
+        if (l + 1 < p.NL) {
+          // a5: hidden epilogue -> next A operand
+          const float* bias = sbias + (l >= 1 ? (l - 1) * H : 0);
+#pragma unroll
+          for (int c = 0; c < H / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(dcol + c * 32, v);
+            tmem_wait_ld();
+            if (l >= 1) {
+              const float4* b4 = reinterpret_cast<const float4*>(bias + c * 32);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 bb = b4[j];
+                v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + bb.x);
+                v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + bb.y);
+                v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + bb.z);
+                v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + bb.w);
+              }
+            }
+            if (PREC == PREC_BF16) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) pk[j] = relu_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+              tmem_st16(acol + c * 16, pk);
+            } else {
+              uint32_t hv[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                float x = fmaxf(__uint_as_float(v[j]), 0.0f);
+                hv[j] = to_tf32(x);
+                if (PREC == PREC_FP32) v[j] = to_tf32(x - __uint_as_float(hv[j]));
+              }
+              tmem_st32(acol + c * 32, hv);
+              if (PREC == PREC_FP32) tmem_st32(acol + H + c * 32, v);
+            }
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[1 + s]);
+        } else {
+          // a7: FP32 final layer, relu(x + b) = max(x, -b) + b folded into c_out
+          float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll
+          for (int c = 0; c < H / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(dcol + c * 32, v);
+            tmem_wait_ld();
+            const float4* w4 = reinterpret_cast<const float4*>(sw + c * 32);
+            const float4* n4 = reinterpret_cast<const float4*>(snb + c * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 w = w4[j], nb = n4[j];
+              acc0 = fmaf(w.x, fmaxf(__uint_as_float(v[4 * j + 0]), nb.x), acc0);
+              acc1 = fmaf(w.y, fmaxf(__uint_as_float(v[4 * j + 1]), nb.y), acc1);
+              acc0 = fmaf(w.z, fmaxf(__uint_as_float(v[4 * j + 2]), nb.z), acc0);
+              acc1 = fmaf(w.w, fmaxf(__uint_as_float(v[4 * j + 3]), nb.w), acc1);
+            }
+          }
+          t = (acc0 + acc1) + p.c_out;
+        }
+      }
+
+      // ---------------- outputs
+      if (mode == MODE_TOPK) {
+        const uint32_t key = f2key(t);
+        // conservative filter on the key alone (a stale or torn read only admits
+        // extra candidates; the merge keeps the exact (key, idx) top-k)
+        const bool pass = valid && key <= ts.misc[2];
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, pass);
+        if (m) {
+          const uint32_t n = __popc(m);
+          if (ncand + n > CAND_CAP) {
+            lock_acquire(ts, lane);
+            warp_merge(ts, mycand, ncand, p.k, lane);
+            lock_release(ts, lane);
+            ncand = 0;
+          }
+          if (pass) {
+            uint32_t pos = ncand + __popc(m & ((1u << lane) - 1u));
+            mycand[pos].idx = I;
+            mycand[pos].key = key;
+            mycand[pos].pad = 0;
+          }
+          ncand += n;
+          __syncwarp();
+        }
+      } else if (valid) {
+        p.t_dense[I - p.begin] = t;
+      }
+      // advance to the slot's next tile
+      I += (uint64_t)p.dTiles * TILE_M;
+      ilo += p.dlo;
+      if (ilo >= p.M_lo) { ilo -= p.M_lo; ++ihi; }
+      ihi += p.dhi;
+    }
+    if (mode == MODE_TOPK && ncand) {
+      lock_acquire(ts, lane);
+      warp_merge(ts, mycand, ncand, p.k, lane);
+      lock_release(ts, lane);
+    }
+  }
+
+  // ---- teardown
+  tc_fence_before();
+  __syncthreads();
+  if (mode == MODE_TOPK) {
+    const surr_record* L = ts.lists + (size_t)ts.misc[1] * p.k;
+    for (uint32_t i = threadIdx.x; i < p.k; i += blockDim.x) p.recs[(size_t)blockIdx.x * p.k + i] = L[i];
+  }
+  if (warp == 0) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ K2
+// Merge `lists` sorted lists of k_in records into the k best (one CTA).
+__global__ void __launch_bounds__(1024, 1)
+    merge_kernel(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k,
+                 uint64_t* out_idx, float* out_t, surr_record* out_recs) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  surr_record* T = reinterpret_cast<surr_record*>(sm);
+  surr_record* N = T + k;
+  surr_record* In = N + k;
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) { T[i].idx = IDX_SENT; T[i].key = KEY_SENT; T[i].pad = 0; }
+  __syncthreads();
+  for (uint32_t j = 0; j < lists; ++j) {
+    const surr_record* src = in + (size_t)j * k_in;
+    for (uint32_t i = threadIdx.x; i < k_in; i += blockDim.x) In[i] = src[i];
+    __syncthreads();
+    const surr_record worst = T[k - 1];
+    if (rec_less(In[0].key, In[0].idx, worst.key, worst.idx)) {
+      for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+        surr_record e = T[i];
+        uint32_t pp = i + lower_bound_recs(In, k_in, e.key, e.idx);
+        if (pp < k) N[pp] = e;
+      }
+      for (uint32_t i = threadIdx.x; i < k_in; i += blockDim.x) {
+        surr_record c = In[i];
+        uint32_t pp = i + lower_bound_recs(T, k, c.key, c.idx);
+        if (pp < k) N[pp] = c;
+      }
+      __syncthreads();
+      surr_record* tmp = T; T = N; N = tmp;
+    }
+    __syncthreads();
+  }
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+    surr_record e = T[i];
+    if (out_idx) out_idx[i] = e.idx;
+    if (out_t) out_t[i] = key2f(e.key);
+    if (out_recs) out_recs[i] = e;
+  }
+}
+
+// ------------------------------------------------------------ decode hook
+struct DecodeParams {
+  uint32_t G, split, M_lo, P;
+  uint32_t R[MAXG], magic[MAXG], shft[MAXG];
+  uint32_t radix[32];
+  uint64_t first, n;
+  uint8_t* out;
+};
+
+__global__ void decode_kernel(const __grid_constant__ DecodeParams p) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t I = p.first + i;
+    uint32_t lo, hi;
+    if (p.split) { hi = (uint32_t)(I / p.M_lo); lo = (uint32_t)(I % p.M_lo); }
+    else { hi = 0; lo = (uint32_t)I; }
+    uint32_t D[MAXG];
+    decode_groups(p, lo, hi, D);
+    for (uint32_t g = 0; g < p.G; ++g) {
+      const uint32_t a = 2 * g, b = 2 * g + 1;
+      const uint32_t rb = b < p.P ? p.radix[b] : 1u;
+      p.out[i * p.P + a] = (uint8_t)(D[g] / rb);
+      if (b < p.P) p.out[i * p.P + b] = (uint8_t)(D[g] % rb);
+    }
+  }
+}
+
+// ------------------------------------------------------------ UMMA self-test
+// One 128 x N x K GEMM: A rows staged to TMEM with tcgen05.st, B bulk-copied
+// to shared memory, D read back with tcgen05.ld.  Test infrastructure for the
+// descriptor / layout encodings the sweep kernel relies on.
+__global__ void __launch_bounds__(128, 1)
+    umma_selftest_kernel(const uint32_t* A, uint32_t K, uint32_t acols, const uint8_t* B, uint32_t bbytes,
+                         float* Dout, uint32_t N, int bf, uint32_t idesc, uint32_t sbo) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ((bbytes + 127u) / 128u) * 128u);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_mbar_init();
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bars[0], bbytes);
+      for (uint32_t off = 0; off < bbytes; off += 32768u)
+        bulk_g2s(smem + off, B + off, min(32768u, bbytes - off), &bars[0]);
+    }
+    __syncwarp();
+    tmem_alloc<512>(tslot);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t base = *tslot;
+  const uint32_t row = threadIdx.x;
+  const uint32_t tl = (warp * 32u) << 16;
+  for (uint32_t c = 0; c < acols; c += 8) {
+    uint32_t v[8];
+    for (int j = 0; j < 8; ++j) v[j] = A[(size_t)row * K + c + j];
+    tmem_st8(base + tl + N + c, v);
+  }
+  tmem_wait_st();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    mbar_wait(&bars[0], 0);
+    tc_fence_after();
+    const uint32_t steps = bf ? K / 16 : K / 8;
+    for (uint32_t kk = 0; kk < steps; ++kk) {
+      const uint64_t d = make_bdesc(smem_u32(smem) + kk * 256u, sbo);
+      if (bf) umma_f16_ts(base, base + N + kk * 8u, d, idesc, kk > 0);
+      else umma_tf32_ts(base, base + N + kk * 8u, d, idesc, kk > 0);
+    }
+    umma_commit(&bars[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bars[1], 0);
+  tc_fence_after();
+  for (uint32_t c = 0; c < N; c += 32) {
+    uint32_t v[32];
+    tmem_ld32(base + tl + c, v);
+    tmem_wait_ld();
+    for (int j = 0; j < 32; ++j) Dout[(size_t)row * N + c + j] = __uint_as_float(v[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(base, 512);
+  }
+}
+
+}  // namespace surr

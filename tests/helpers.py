@@ -1,0 +1,59 @@
+"""Shared test utilities: tolerances and the G17 top-k acceptance rule."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+# Relative-error bounds on t (rel = |dt| / max(|t|, 1e-3 sigma_y)).
+#  fp32 : 3xTF32 hidden layers + FP32 final       -> north star 1e-5
+#  tf32 : 1xTF32 hidden layers, 3xTF32 first layer -> north star's 1e-3 bound
+#  bf16 : BF16 hidden layers; the trained nets
+#         reach 2.6e-3 (cfg2) .. 4.6e-3 (cfg5) in the rounding emulation, so
+#         the bound derived from the arithmetic is 1e-2 (not 1e-3).
+TOL = {"fp32": 1e-5, "tf32": 1e-3, "bf16": 1e-2}
+
+
+def rel_err(t_gpu, t_ref, y_scale):
+    t_gpu = np.asarray(t_gpu, np.float64)
+    t_ref = np.asarray(t_ref, np.float64)
+    den = np.maximum(np.abs(t_ref), 1e-3 * abs(y_scale) + 1e-30)
+    return np.abs(t_gpu - t_ref) / den
+
+
+def check_topk(gpu_idx, gpu_t, ref_idx, ref_t, eval_ref, tol, y_scale):
+    """(i) every GPU item's time is within tol of the oracle's time
+    for that index; (ii) items only on one side lie in the tie band around the
+    oracle's k-th time; (iii) order inversions only inside the band."""
+    gpu_idx = np.asarray(gpu_idx, np.uint64)
+    ref_idx = np.asarray(ref_idx, np.uint64)
+    assert len(gpu_idx) == len(ref_idx)
+    assert len(set(gpu_idx.tolist())) == len(gpu_idx), "duplicate indices in GPU top-k"
+    t_at = eval_ref(gpu_idx)
+    e = rel_err(gpu_t, t_at, y_scale)
+    assert e.max() <= tol, f"(i) max rel err {e.max():.3e} > {tol}"
+    Tk = float(np.max(ref_t))
+    band = tol * max(abs(Tk), 1e-3 * abs(y_scale)) * 2.0
+    only_gpu = set(gpu_idx.tolist()) - set(ref_idx.tolist())
+    only_ref = set(ref_idx.tolist()) - set(gpu_idx.tolist())
+    ref_map = dict(zip(ref_idx.tolist(), np.asarray(ref_t).tolist()))
+    gpu_map = dict(zip(gpu_idx.tolist(), t_at.tolist()))
+    for i in only_gpu:
+        assert gpu_map[i] <= Tk + band, f"(ii) GPU-only item {i} t={gpu_map[i]} > Tk={Tk}"
+    for i in only_ref:
+        assert ref_map[i] >= Tk - band, f"(ii) oracle-only item {i} t={ref_map[i]} < Tk={Tk}"
+    for a, b in zip(t_at[:-1], t_at[1:]):
+        assert a <= b + band, f"(iii) order inversion {a} > {b}"
+    return len(only_gpu)
+
+
+def need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2306_14011_b200 as pk
+    if not os.path.exists(pk.LIB_PATH):
+        pk.build_library()
+    return pk

@@ -1,0 +1,182 @@
+"""GPU path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Sizes: the tiny space in full; cfg2 (15^7) on ragged sub-ranges spanning many
+tiles; full-size sweeps checked by re-evaluating every returned item with the
+oracle and by the closed-form pins (all-ties net, affine net).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import workloads
+from oracle import space as ospace
+from oracle import sweep as osweep
+from tests import pins
+from tests.helpers import TOL, check_topk, need_gpu, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pk():
+    return need_gpu()
+
+
+def _handle(pk, model, prec):
+    return pk.Surrogate(0).load(model, prec)
+
+
+# ------------------------------------------------------------------ decode (a2)
+@pytest.mark.parametrize("name,first,n", [("tiny", 0, 2 ** 14), ("cfg2", 0, 1 << 16),
+                                          ("cfg2", 170859375 - 5000, 5000), ("cfg5", 13492928512 - 70000, 70000),
+                                          ("cfg5", 7_000_000_123, 100000), ("paper", 358318080000000 - 4096, 4096),
+                                          ("paper", 123456789012345, 65536)])
+def test_decode_bit_exact(pk, name, first, n):
+    vl = workloads.space(name)
+    model = workloads.random_net(vl, [32, 32], seed=1)
+    h = _handle(pk, model, "bf16")
+    got = h.decode_range(vl, first, n).cpu().numpy().astype(np.int64)
+    ref = ospace.decode(np.arange(first, first + n, dtype=np.uint64), workloads.radices(name))
+    assert np.array_equal(got, ref)
+
+
+# ------------------------------------------------------------------ dense t(I)
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+def test_tiny_all_times(pk, prec):
+    vl = workloads.space("tiny")
+    model = workloads.load_model("tiny_14-32-32-1")
+    h = _handle(pk, model, prec)
+    t = h.eval_range(vl, 0, 2 ** 14).cpu().numpy()
+    ref = osweep.times(model, vl, 0, 2 ** 14)
+    e = rel_err(t, ref, model["y_scale"])
+    assert e.max() <= TOL[prec], f"{prec}: max rel err {e.max():.3e}"
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("begin,n", [(0, 1 << 18), (98_765_431, (1 << 18) + 77), (170859375 - 100003, 100003)])
+def test_cfg2_slice_times(pk, prec, begin, n):
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, prec)
+    t = h.eval_range(vl, begin, begin + n).cpu().numpy()
+    ref = osweep.times(model, vl, begin, begin + n)
+    e = rel_err(t, ref, model["y_scale"])
+    assert e.max() <= TOL[prec], f"{prec}: max rel err {e.max():.3e} at {begin + int(np.argmax(e))}"
+
+
+def test_predict_matches_oracle_and_sweep_bitwise(pk):
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    for prec in ["bf16", "fp32"]:
+        h = _handle(pk, model, prec)
+        # rows = configs [b, b+n) so predict and the dense sweep see identical inputs
+        b, n = 5_000_017, 3001
+        X = ospace.values_of(ospace.decode(np.arange(b, b + n, dtype=np.uint64), workloads.radices("cfg2")), vl)
+        tp = h.predict(torch.tensor(X, dtype=torch.float32, device="cuda:0")).cpu().numpy()
+        ts = h.eval_range(vl, b, b + n).cpu().numpy()
+        assert np.array_equal(tp, ts)
+        e = rel_err(tp, osweep.times(model, vl, b, b + n), model["y_scale"])
+        assert e.max() <= TOL[prec]
+        assert h.predict(torch.zeros((0, 14), dtype=torch.float32, device="cuda:0")).numel() == 0
+
+
+# ------------------------------------------------------------------ top-k
+def test_tiny_top1_exact_fp32(pk):
+    vl = workloads.space("tiny")
+    model = workloads.load_model("tiny_14-32-32-1")
+    h = _handle(pk, model, "fp32")
+    idx, t, cnt = h.sweep(vl, 1)
+    ri, rt = osweep.topk(model, vl, 1)
+    assert cnt == 1 and int(idx[0]) == int(ri[0])
+    assert rel_err(t.cpu().numpy(), rt, model["y_scale"]).max() <= TOL["fp32"]
+
+
+@pytest.mark.parametrize("prec,k", [("fp32", 16), ("bf16", 16), ("tf32", 64), ("bf16", 1024), ("fp32", 1000)])
+def test_cfg2_subrange_topk(pk, prec, k):
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, prec)
+    b, e = 33_333_333, 33_333_333 + (1 << 21) + 55
+    idx, t, cnt = h.sweep(vl, k, b, e)
+    ri, rt = osweep.topk(model, vl, k, b, e)
+    assert cnt == k
+    check_topk(idx.cpu().numpy().astype(np.uint64), t.cpu().numpy(), ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_cfg2_full_sweep_reevaluated(pk, prec):
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, prec)
+    idx, t, cnt = h.sweep(vl, 16)
+    idx = idx.cpu().numpy().astype(np.uint64)
+    t = t.cpu().numpy()
+    assert cnt == 16 and np.all(np.diff(t) >= 0)
+    e = rel_err(t, osweep.times_at(model, vl, idx), model["y_scale"])
+    assert e.max() <= TOL[prec]
+
+
+def test_all_ties_net_full_size(pk):
+    vl = workloads.space("cfg5")
+    model = workloads.all_ties_net(vl, [128, 128])
+    h = _handle(pk, model, "bf16")
+    b = 9_000_000_000
+    idx, t, _ = h.sweep(vl, 64, b, b + 3_000_000)
+    assert idx.cpu().numpy().tolist() == list(range(b, b + 64))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_affine_net_closed_form_full_cfg5(pk, prec):
+    vl = workloads.space("cfg5")
+    model = workloads.affine_net(vl, [128, 128], seed=11)
+    h = _handle(pk, model, prec)
+    k = 256
+    idx, t, _ = h.sweep(vl, k)
+    ci, ct = pins.affine_kbest(model, vl, k)
+    C, tables = pins.affine_tables(model, vl)
+    digits = ospace.decode(idx.cpu().numpy().astype(np.uint64), workloads.radices("cfg5"))
+
+    def closed(ii):
+        d = ospace.decode(np.asarray(ii, np.uint64), workloads.radices("cfg5"))
+        return C + sum(tables[j][d[:, j]] for j in range(14))
+
+    assert digits.shape == (k, 14)
+    check_topk(idx.cpu().numpy().astype(np.uint64), t.cpu().numpy(), np.array(ci, np.uint64), np.array(ct),
+               closed, TOL[prec], model["y_scale"])
+
+
+def test_edge_cases(pk):
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, "bf16")
+    # empty range
+    idx, t, cnt = h.sweep(vl, 8, 1000, 1000)
+    assert cnt == 0
+    # k larger than the range, ragged single partial tile
+    idx, t, cnt = h.sweep(vl, 50, 1000, 1007)
+    assert cnt == 7 and sorted(idx[:7].cpu().tolist()) == list(range(1000, 1007))
+    assert np.all(idx[7:].cpu().numpy() == -1)
+    # invalid arguments raise
+    with pytest.raises(pk.SurrogateError):
+        h.sweep(vl, 0)
+    with pytest.raises(pk.SurrogateError):
+        h.sweep(vl, 2000)
+    with pytest.raises(pk.SurrogateError):
+        h.sweep(vl, 4, 10, 5)
+
+
+def test_shard_invariance_bitwise(pk):
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, "bf16")
+    b, e, k = 1_000_000, 1_000_000 + 4_000_003, 32
+    full_i, full_t, _ = h.sweep(vl, k, b, e)
+    for W in (2, 3, 8):
+        recs = []
+        for r in range(W):
+            lo, hi = ospace.shard(e - b, W, r)
+            recs.append(h.sweep_records(vl, k, b + lo, b + hi))
+        mi, mt, _ = h.merge_topk(torch.cat(recs), W, k, k)
+        assert torch.equal(mi, full_i) and torch.equal(mt, full_t)
