@@ -1,0 +1,297 @@
+#!/usr/bin/env python3
+"""Benchmark of the exhaustive surrogate sweep (BASELINE.json metric: surrogate
+evals/sec over the 14-parameter space; % tensor-pipe peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
+                    [--precision bf16|tf32|fp32] [--impl ours|reference]
+
+One step = one pass of the whole hot path over the workload's index range:
+K1 (decode + normalise + fused MLP + block top-k) and K2 (grid merge); with
+N > 1 ranks each sweep a contiguous shard, the per-rank
+top-k records are exchanged with ONE NCCL all_gather and merged by K2 on
+every rank (a10).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, float64 numpy) on a bounded
+sample of the same workload; it is the deliberately slow reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+PEAK_RATIO = {"bf16": 1.0, "tf32": 0.5, "fp32": 0.5}   # nominal dense tf32 / bf16 = 1.1 / 2.25 PF
+
+
+def algorithmic_flops(widths):
+    """2 * MACs per config of the FCNN (the K padding and 3xTF32 passes excluded)."""
+    return 2 * sum(a * b for a, b in zip(widths[:-1], widths[1:]))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 1590.0, 1400.0, "fallback"
+
+
+def ncu_traffic(workload, precision):
+    """Per-launch DRAM bytes of K1 from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(f"{workload}/{precision}")
+        return None if e is None else e.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        loaded = [r for r in rows if r[0] > 300] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in loaded for n, v in zip(names, r[2]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(loaded)}
+
+
+def run_reference(args, wl, rank):
+    """The CPU oracle, as it stands, on a bounded sample of the workload."""
+    if rank != 0:
+        return
+    import threadpoolctl
+
+    from oracle import sweep as osweep
+    vl = workloads.space(wl.space)
+    model = workloads.load_model(wl.weights)
+    N = int(np.prod([len(v) for v in vl]))
+    sample = 1 << 18
+    lo = N // 3
+    osweep.topk(model, vl, wl.k, lo, lo + 4096)  # warm-up
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        osweep.topk(model, vl, wl.k, lo + s * sample, lo + (s + 1) * sample)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    cores = max(i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()) or 1
+    value = sample / statistics.median(times)
+    out = {"impl": "reference", "metric": "surrogate evals/sec over the 14-param space", "value": value,
+           "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": wl.name, "space": f"{N} configs", "net": "-".join(map(str, model["widths"])),
+                      "k": wl.k, "precision": "fp64 (oracle)", "sample": f"{sample} consecutive configs per step"},
+           "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                            "sample": f"{sample} configs/step at offset |S|/3, numpy float64"},
+           "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(wl, model, vl, budget_s=12.0):
+    import threadpoolctl
+
+    from oracle import sweep as osweep
+    N = int(np.prod([len(v) for v in vl]))
+    chunk = 1 << 17
+    lo = N // 2
+    osweep.topk(model, vl, wl.k, lo, lo + 2048)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        osweep.topk(model, vl, wl.k, lo + done, lo + done + chunk, chunk=chunk)
+        done += chunk
+    dt = time.perf_counter() - t0
+    cores = max(i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()) or 1
+    return {"value": done / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+            "sample": f"{done} consecutive configs of {wl.name} from |S|/2 ({dt:.1f} s, numpy float64 top-k)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--precision", default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = workloads.WORKLOADS[args.workload]
+    precision = args.precision or wl.precision
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, wl, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_14011_b200 as pk
+    from paper_2306_14011_b200.dist import shard_range
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    vl = workloads.space(wl.space)
+    model = workloads.load_model(wl.weights)
+    N = int(np.prod([len(v) for v in vl]))
+    lo, hi = shard_range(N, world, rank)
+    h = pk.Surrogate(local).load(model, precision)
+    k = wl.k
+    dev = torch.device(f"cuda:{local}")
+    desc = pk.SpaceDesc(vl, lo, hi)
+    stream = torch.cuda.current_stream()
+    idx = torch.empty(k, dtype=torch.int64, device=dev)
+    tt = torch.empty(k, dtype=torch.float32, device=dev)
+    recs = torch.empty((k, 2), dtype=torch.int64, device=dev)
+    gathered = torch.empty((world * k, 2), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        if world == 1:
+            h.sweep_into(desc, k, idx, tt)
+            return h.last_launches()
+        n = h.sweep_records_into(desc, k, recs)
+        dist.all_gather_into_tensor(gathered, recs)
+        h.merge_topk_into(gathered, world, k, k, idx, tt)
+        return n + h.last_launches()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    h.kernel_timing(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.zero_()                      # L2 flushed between timed steps (untimed)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev[s][0].record(stream)
+            launches += step()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    k1_ms, k1_n = h.kernel_timing_get()
+    h.kernel_timing(False)
+    if world > 1:
+        tms = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        total_ms = float(tms.item())
+    value = N * args.steps / (total_ms / 1e3)
+    # roofline of the dominant kernel (K1) from its own CUDA events on the launch stream
+    k1_avg_s = (k1_ms / max(k1_n, 1)) / 1e3
+    flops = algorithmic_flops(model["widths"]) * (hi - lo)
+    achieved = flops / k1_avg_s / 1e12
+    burst, sustained, src = load_peaks()
+    peak = burst * PEAK_RATIO[precision]
+    traffic = ncu_traffic(wl.name, precision)
+
+    # end to end through the public API: value table H2D + result D2H every step
+    e2e = None
+    if world == 1:
+        hidx, ht = np.empty(k, np.uint64), np.empty(k, np.float32)
+        for _ in range(2):
+            h.sweep_host(vl, k, desc=desc, out=(hidx, ht))
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            h.sweep_host(vl, k, desc=desc, out=(hidx, ht))
+        e2e_s = time.perf_counter() - t0
+        lut_bytes = h.lut_bytes()
+        e2e = {"value": N * args.steps / e2e_s, "unit": "evals/s",
+               "h2d_bytes_per_step": int(lut_bytes + desc.radix.nbytes + desc.values.nbytes),
+               "d2h_bytes_per_step": int(k * (8 + 4))}
+
+    if rank == 0:
+        out = {"metric": "surrogate evals/sec over the 14-param space", "value": value, "unit": "evals/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": precision, "data": "synthetic",
+               "config": {"workload": wl.name, "space": f"{wl.space}: {N} configs",
+                          "net": "-".join(map(str, model["widths"])), "k": k, "precision": precision,
+                          "weights": f"oracle-trained ({wl.weights})",
+                          "l2": "flushed between timed steps (256 MiB write, untimed); inputs generated on chip",
+                          "parallelism": f"dp{world} (index-range shards, 1 all_gather + merge)"},
+               "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                            "frac": achieved / peak, "traffic": traffic,
+                            "peak_source": f"{src} bf16 burst x {PEAK_RATIO[precision]} ({precision})",
+                            "kernel": "sweep_kernel (K1)", "k1_ms": k1_avg_s * 1e3,
+                            "flops_per_config": algorithmic_flops(model["widths"])},
+               "e2e": e2e, "gpu_launches": launches}
+        with_clk = clk.summary()
+        out["clocks"] = with_clk
+        if not args.no_cpu_baseline and world == 1:
+            out["cpu_baseline"] = cpu_baseline(wl, model, vl)
+        elif not args.no_cpu_baseline:
+            out["cpu_baseline"] = None
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

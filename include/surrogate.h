@@ -167,6 +167,10 @@ surr_status surrogate_space_size(const surr_space *space, uint64_t *out);
 surr_status surrogate_kernel_timing(surrogate_t *h, int enable);
 surr_status surrogate_kernel_timing_get(surrogate_t *h, double *total_ms, uint32_t *launches);
 
+/* Bytes of the value lookup table of the cached space (the per-sweep H2D of
+ * surrogate_sweep_host). */
+uint32_t surrogate_table_bytes(const surrogate_t *h);
+
 /* Number of kernel launches the last call issued on the GPU (for the bench's
  * gpu_launches count). */
 uint32_t surrogate_last_launches(const surrogate_t *h);

@@ -23,7 +23,7 @@ EXPORTS = [
     "surrogate_predict", "surrogate_sweep", "surrogate_sweep_host", "surrogate_eval_range",
     "surrogate_merge_topk", "surrogate_sweep_records", "surrogate_decode_range", "surrogate_space_size",
     "surrogate_kernel_timing", "surrogate_kernel_timing_get", "surrogate_last_launches",
-    "surrogate_selftest_umma",
+    "surrogate_selftest_umma", "surrogate_table_bytes",
 ]
 
 
@@ -77,6 +77,8 @@ def lib() -> ctypes.CDLL:
         L.surrogate_last_launches.argtypes = [vp]
         L.surrogate_last_launches.restype = u32
         L.surrogate_selftest_umma.argtypes = [i32, i32, u32, u32, vp, vp, vp]
+        L.surrogate_table_bytes.argtypes = [vp]
+        L.surrogate_table_bytes.restype = u32
         for name in EXPORTS:
             fn = getattr(L, name)
             if fn.restype is ctypes.c_int and name not in ("surrogate_last_launches",):
@@ -221,6 +223,20 @@ class Surrogate:
                                           ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(t.data_ptr()),
                                           ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)), self.h)
         return idx, t, out
+
+    def sweep_records_into(self, desc: SpaceDesc, k: int, recs, stream=None) -> int:
+        _check(lib().surrogate_sweep_records(self.h, ctypes.byref(desc.c), k, ctypes.c_void_p(recs.data_ptr()),
+                                             _stream_ptr(stream)), self.h)
+        return self.last_launches()
+
+    def merge_topk_into(self, recs, lists: int, k_in: int, k: int, idx, t, stream=None):
+        _check(lib().surrogate_merge_topk(self.h, ctypes.c_void_p(recs.data_ptr()), lists, k_in, k,
+                                          ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(t.data_ptr()),
+                                          None, _stream_ptr(stream)), self.h)
+
+    def lut_bytes(self) -> int:
+        """Bytes of the value table uploaded by the last sweep (the per-step H2D)."""
+        return int(lib().surrogate_table_bytes(self.h))
 
     def eval_range(self, value_lists, begin: int, end: int, stream=None):
         """t(I) for every I in [begin, end) from the fused kernel (dense mode)."""

@@ -435,6 +435,8 @@ const char* surrogate_last_error(const surrogate_t* h) { return h ? h->err.c_str
 
 uint32_t surrogate_last_launches(const surrogate_t* h) { return h ? h->launches : 0; }
 
+uint32_t surrogate_table_bytes(const surrogate_t* h) { return h && h->space_valid ? h->sp.lut_bytes : 0; }
+
 surr_status surrogate_space_size(const surr_space* sp, uint64_t* out) {
   surrogate* h = nullptr;
   if (!sp || !out || !sp->radix) return fail(h, SURR_E_INVALID_ARG, "null argument");
@@ -554,6 +556,9 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     cacc += Wout[n] * bj;
   }
   p.c_out = (float)(m->y_mean + m->y_scale * cacc);
+  for (uint32_t n = 0; n < H; ++n) { p.fin_w[n] = fw[n]; p.fin_nb[n] = fnb[n]; }
+  for (uint32_t l = 1; l + 1 < NL; ++l)
+    for (uint32_t n = 0; n < H; ++n) p.hbias[l - 1][n] = (float)m->b[l][n];
   p.NL = NL;
   p.sbo_b1 = (K0 / (16 / esz)) * 128;
   p.sbo_bh = (H / (16 / esz)) * 128;

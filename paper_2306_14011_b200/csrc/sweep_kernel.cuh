@@ -61,6 +61,11 @@ struct KParams {
   uint32_t sbo_b1, sbo_bh;
   uint32_t idesc_l1, idesc_h;
   float c_out;
+  // epilogue constants in the kernel-parameter (constant) bank: used directly
+  // as instruction operands, no shared-memory traffic
+  float fin_w[128];         // y_scale * w_out
+  float fin_nb[128];        // -b of the last hidden layer (0 when it is layer 1)
+  float hbias[2][128];      // biases of model layers 2 .. NL-1 (hidden epilogues)
   // outputs
   uint32_t k;
   surr_record* recs;        // MODE_TOPK: gridDim.x * k records
@@ -209,7 +214,61 @@ __device__ __forceinline__ void lock_release(TopkShared& ts, uint32_t lane) {
   }
 }
 
-// ---------------------------------------------------------------- kernel
+
+// A0 operand of one row: bf16 -> 8 packed columns; tf32 -> 16 hi + 16 lo slots.
+struct A0Regs {
+  uint32_t hi[K0], lo[K0];
+};
+
+template <int PREC>
+__device__ __forceinline__ void make_a0_sweep(const KParams& p, const uint8_t* slut, uint32_t ilo, uint32_t ihi,
+                                              A0Regs& a) {
+  uint32_t D[MAXG];
+  decode_groups(p, ilo, ihi, D);
+#pragma unroll
+  for (int g = 0; g < MAXG; ++g) {
+    if (g < (int)p.G) {
+      if (PREC == PREC_BF16) {
+        a.hi[g] = reinterpret_cast<const uint32_t*>(slut)[p.lut_off[g] + D[g]];
+      } else {
+        const uint4 e = reinterpret_cast<const uint4*>(slut)[p.lut_off[g] + D[g]];
+        a.hi[2 * g] = e.x; a.hi[2 * g + 1] = e.y; a.lo[2 * g] = e.z; a.lo[2 * g + 1] = e.w;
+      }
+    } else {
+      if (PREC == PREC_BF16) {
+        a.hi[g] = p.a0_const[g];
+      } else {
+        a.hi[2 * g] = p.a0_const[2 * g]; a.hi[2 * g + 1] = p.a0_const[2 * g + 1];
+        a.lo[2 * g] = p.a0_const[K0 + 2 * g]; a.lo[2 * g + 1] = p.a0_const[K0 + 2 * g + 1];
+      }
+    }
+  }
+}
+
+// explicit-batch rows: z_j = (x_j - shift_j) / scale_j in double (identical to
+// the host table), slot P = 1 (bias), rest 0
+template <int PREC>
+__device__ __forceinline__ void make_a0_predict(const KParams& p, uint64_t r, A0Regs& a) {
+  const float* xr = p.x + r * p.P;
+  float z[K0];
+#pragma unroll
+  for (int j = 0; j < K0; ++j) {
+    z[j] = 0.0f;
+    if (j < (int)p.P) z[j] = __double2float_rn(((double)__ldg(xr + j) - p.zshift[j]) / p.zscale[j]);
+    else if (j == (int)p.P) z[j] = 1.0f;
+  }
+  if (PREC == PREC_BF16) {
+#pragma unroll
+    for (int c = 0; c < K0 / 2; ++c) a.hi[c] = bf16x2(z[2 * c], z[2 * c + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K0; ++j) {
+      a.hi[j] = to_tf32(z[j]);
+      a.lo[j] = to_tf32(z[j] - __uint_as_float(a.hi[j]));
+    }
+  }
+}
+
 template <int PREC, int H>
 __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
     sweep_kernel(const __grid_constant__ KParams p, int mode) {
@@ -230,20 +289,17 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
     if (lane == 0) {
       mbar_init(&bars[0], 1);
       for (int s = 0; s < C::NSLOT; ++s) {
-        mbar_init(&bars[1 + s], 4);  // one arrive per epilogue warp
+        mbar_init(&bars[1 + s], 4);  // one arrive per epilogue warp of the slot
         mbar_init(&bars[3 + s], 1);  // tcgen05.commit
       }
       fence_mbar_init();
       fence_proxy_async_smem();
-      // weights (+ LUT) -> smem through the bulk-copy engine, one mbarrier
-      uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
+      // weights (+ value table) -> smem through the bulk-copy engine, one mbarrier
+      const uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
       mbar_arrive_expect_tx(&bars[0], total);
-      for (uint32_t off = 0; off < p.w_bytes; off += 32768u) {
-        uint32_t n = min(32768u, p.w_bytes - off);
-        bulk_g2s(smem + off, (const uint8_t*)p.w_gmem + off, n, &bars[0]);
-      }
-      if (mode != MODE_PREDICT && p.lut_bytes)
-        bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[0]);
+      for (uint32_t off = 0; off < p.w_bytes; off += 32768u)
+        bulk_g2s(smem + off, (const uint8_t*)p.w_gmem + off, min(32768u, p.w_bytes - off), &bars[0]);
+      if (mode != MODE_PREDICT && p.lut_bytes) bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[0]);
     }
     __syncwarp();
     tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -264,51 +320,52 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
 
   if (warp == 0) {
     // ================= UMMA issuer (one thread) =================
+    // Round-robin over slots, layer by layer; every wait is a blocking
+    // (HW-suspending) try_wait so the issuer takes no issue slots from the
+    // epilogue warps sharing its SM sub-partition.
     if (lane == 0) {
       mbar_wait(&bars[0], 0);  // weights resident
-      uint32_t left[C::NSLOT], layer[C::NSLOT], ph[C::NSLOT];
-      uint32_t active = 0;
+      uint32_t ntile[C::NSLOT], ph[C::NSLOT];
+      uint32_t rounds = 0;
       for (int s = 0; s < C::NSLOT; ++s) {
-        uint64_t t0 = (uint64_t)blockIdx.x * C::NSLOT + s;
-        left[s] = t0 < p.num_tiles ? (uint32_t)((p.num_tiles - t0 - 1) / p.dTiles + 1) : 0u;
-        layer[s] = 0;
+        const uint64_t t0 = (uint64_t)blockIdx.x * C::NSLOT + s;
+        ntile[s] = t0 < p.num_tiles ? (uint32_t)((p.num_tiles - t0 - 1) / p.dTiles + 1) : 0u;
         ph[s] = 0;
-        active += left[s] ? 1u : 0u;
+        rounds = max(rounds, ntile[s]);
       }
       const uint32_t sb = smem_u32(smem);
-      while (active) {
+      for (uint32_t j = 0; j < rounds; ++j) {
+        for (uint32_t l = 0; l < p.NL; ++l) {
 #pragma unroll
-        for (int s = 0; s < C::NSLOT; ++s) {
-          if (!left[s] || !mbar_test(&bars[1 + s], ph[s])) continue;
-          ph[s] ^= 1u;
-          tc_fence_after();
-          const uint32_t d = tmem_base + s * C::SLOT_COLS;
-          const uint32_t a = d + H;
-          const uint32_t l = layer[s];
-          uint32_t bhi, blo, sbo, idesc, steps, passes, alo;
-          if (l == 0) {
-            bhi = sb + p.off_b1; blo = sb + p.off_b1lo; sbo = p.sbo_b1; idesc = p.idesc_l1;
-            steps = PREC == PREC_BF16 ? K0 / 16 : K0 / 8; passes = C::PASSES_1; alo = a + C::A0_LO;
-          } else {
-            bhi = sb + p.off_bh + (l - 1) * p.stride_bh; blo = bhi + p.lo_delta_h; sbo = p.sbo_bh;
-            idesc = p.idesc_h; steps = PREC == PREC_BF16 ? H / 16 : H / 8; passes = C::PASSES_H; alo = a + H;
-          }
-          for (uint32_t kk = 0; kk < steps; ++kk) {
-            const uint64_t dh = make_bdesc(bhi + kk * 256u, sbo);
-            if (PREC == PREC_BF16) {
-              umma_f16_ts(d, a + kk * 8u, dh, idesc, kk > 0);
+          for (int s = 0; s < C::NSLOT; ++s) {
+            if (j >= ntile[s]) continue;
+            mbar_wait(&bars[1 + s], ph[s]);
+            ph[s] ^= 1u;
+            tc_fence_after();
+            const uint32_t d = tmem_base + s * C::SLOT_COLS;
+            const uint32_t a = d + H;
+            uint32_t bhi, blo, sbo, idesc, steps, alo;
+            bool three;
+            if (l == 0) {
+              bhi = sb + p.off_b1; blo = sb + p.off_b1lo; sbo = p.sbo_b1; idesc = p.idesc_l1;
+              steps = PREC == PREC_BF16 ? K0 / 16 : K0 / 8; three = C::PASSES_1 == 3; alo = a + C::A0_LO;
             } else {
-              umma_tf32_ts(d, a + kk * 8u, dh, idesc, kk > 0);
-              if (passes == 3) {
-                umma_tf32_ts(d, a + kk * 8u, make_bdesc(blo + kk * 256u, sbo), idesc, 1u);
-                umma_tf32_ts(d, alo + kk * 8u, dh, idesc, 1u);
+              bhi = sb + p.off_bh + (l - 1) * p.stride_bh; blo = bhi + p.lo_delta_h; sbo = p.sbo_bh;
+              idesc = p.idesc_h; steps = PREC == PREC_BF16 ? H / 16 : H / 8; three = C::PASSES_H == 3; alo = a + H;
+            }
+            for (uint32_t kk = 0; kk < steps; ++kk) {
+              const uint64_t dh = make_bdesc(bhi + kk * 256u, sbo);
+              if (PREC == PREC_BF16) {
+                umma_f16_ts(d, a + kk * 8u, dh, idesc, kk > 0);
+              } else {
+                umma_tf32_ts(d, a + kk * 8u, dh, idesc, kk > 0);
+                if (three) {
+                  umma_tf32_ts(d, a + kk * 8u, make_bdesc(blo + kk * 256u, sbo), idesc, 1u);
+                  umma_tf32_ts(d, alo + kk * 8u, dh, idesc, 1u);
+                }
               }
             }
-          }
-          umma_commit(&bars[3 + s]);
-          if (++layer[s] == p.NL) {
-            layer[s] = 0;
-            if (--left[s] == 0) --active;
+            umma_commit(&bars[3 + s]);
           }
         }
       }
@@ -321,9 +378,6 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
     const uint32_t tl = (wq * 32u) << 16;  // TMEM lane offset of this warp
     const uint32_t dcol = tmem_base + tl + s * C::SLOT_COLS;
     const uint32_t acol = dcol + H;
-    const float* sbias = reinterpret_cast<const float*>(smem + p.off_bias);
-    const float* snb = reinterpret_cast<const float*>(smem + p.off_nb);
-    const float* sw = reinterpret_cast<const float*>(smem + p.off_w);
     const uint8_t* slut = smem + p.smem_lut;
     surr_record* mycand = ts.cand + (size_t)(warp - 4) * CAND_CAP;
     uint32_t ncand = 0;
@@ -333,108 +387,81 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
     uint32_t ilo, ihi;
     if (p.split) { ihi = (uint32_t)(I / p.M_lo); ilo = (uint32_t)(I % p.M_lo); }
     else { ihi = 0; ilo = (uint32_t)I; }
+    const uint64_t dI = (uint64_t)p.dTiles * TILE_M;
     uint32_t phd = 0;
-    mbar_wait(&bars[0], 0);  // LUT / weights resident
+    mbar_wait(&bars[0], 0);  // table / weights resident
 
+    // software pipeline: the A0 operand of the NEXT tile is decoded while the
+    // last UMMA layer of the current tile runs
+    A0Regs a0;
+    if (tile < p.num_tiles) {
+      if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, I < p.end ? I : p.begin, a0);
+      else make_a0_sweep<PREC>(p, slut, ilo, ihi, a0);
+    }
     for (; tile < p.num_tiles; tile += p.dTiles) {
       const bool valid = I < p.end;
-      // ---------------- a2 + a3: A0 operand
-      uint32_t hi16[K0], lo16[K0];  // tf32: hi/lo slots; bf16: hi16[0..7] = packed columns
-      if (mode == MODE_PREDICT) {
-        // z_j = (x_j - shift_j) / scale_j in double (identical to the host LUT), slot P = 1
-        const uint64_t r = valid ? I : p.begin;
-        const float* xr = p.x + r * p.P;
-        float z[K0];
-#pragma unroll
-        for (int j = 0; j < K0; ++j) {
-          z[j] = 0.0f;
-          if (j < (int)p.P) z[j] = __double2float_rn(((double)xr[j] - p.zshift[j]) / p.zscale[j]);
-          else if (j == (int)p.P) z[j] = 1.0f;
-        }
-        if (PREC == PREC_BF16) {
-#pragma unroll
-          for (int c = 0; c < K0 / 2; ++c)
-            hi16[c] = bf16x2(z[2 * c], z[2 * c + 1]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < K0; ++j) {
-            hi16[j] = to_tf32(z[j]);
-            lo16[j] = to_tf32(z[j] - __uint_as_float(hi16[j]));
-          }
-        }
-      } else {
-        uint32_t D[MAXG];
-        decode_groups(p, ilo, ihi, D);
-#pragma unroll
-        for (int g = 0; g < MAXG; ++g) {
-          if (g < (int)p.G) {
-            if (PREC == PREC_BF16) {
-              hi16[g] = reinterpret_cast<const uint32_t*>(slut)[p.lut_off[g] + D[g]];
-            } else {
-              const uint4 e = reinterpret_cast<const uint4*>(slut)[p.lut_off[g] + D[g]];
-              hi16[2 * g] = e.x; hi16[2 * g + 1] = e.y; lo16[2 * g] = e.z; lo16[2 * g + 1] = e.w;
-            }
-          } else {
-            if (PREC == PREC_BF16) {
-              hi16[g] = p.a0_const[g];
-            } else {
-              hi16[2 * g] = p.a0_const[2 * g]; hi16[2 * g + 1] = p.a0_const[2 * g + 1];
-              lo16[2 * g] = p.a0_const[K0 + 2 * g]; lo16[2 * g + 1] = p.a0_const[K0 + 2 * g + 1];
-            }
-          }
-        }
-      }
+      // ---------------- a2 + a3: A0 operand -> TMEM
       if (PREC == PREC_BF16) {
-        tmem_st8(acol, hi16);
+        tmem_st8(acol, a0.hi);
       } else {
-        tmem_st16(acol, hi16);
-        tmem_st16(acol + C::A0_LO, lo16);
+        tmem_st16(acol, a0.hi);
+        tmem_st16(acol + C::A0_LO, a0.lo);
       }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[1 + s]);
 
+      // next tile's row index (and its A0, computed below)
+      const uint64_t In = I + dI;
+      uint32_t nlo = ilo + p.dlo, nhi = ihi + p.dhi;
+      if (nlo >= p.M_lo) { nlo -= p.M_lo; ++nhi; }
+      const bool has_next = tile + p.dTiles < p.num_tiles;
+
       // ---------------- layers
       float t = 0.0f;
       for (uint32_t l = 0; l < p.NL; ++l) {
+        if (l + 1 == p.NL && has_next) {
+          if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
+          else make_a0_sweep<PREC>(p, slut, nlo, nhi, a0);
+        }
         mbar_wait(&bars[3 + s], phd);
         phd ^= 1u;
         tc_fence_after();
         if (l + 1 < p.NL) {
-          // a5: hidden epilogue -> next A operand
-          const float* bias = sbias + (l >= 1 ? (l - 1) * H : 0);
+          // a5: hidden epilogue -> next A operand (two 32-column chunks per TMEM wait)
 #pragma unroll
-          for (int c = 0; c < H / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld32(dcol + c * 32, v);
+          for (int c = 0; c < H / 32; c += 2) {
+            uint32_t v[2][32];
+            tmem_ld32(dcol + c * 32, v[0]);
+            if (H / 32 > 1) tmem_ld32(dcol + (c + 1) * 32, v[1]);
             tmem_wait_ld();
-            if (l >= 1) {
-              const float4* b4 = reinterpret_cast<const float4*>(bias + c * 32);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 bb = b4[j];
-                v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + bb.x);
-                v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + bb.y);
-                v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + bb.z);
-                v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + bb.w);
+            for (int u = 0; u < 2; ++u) {
+              if (u == 1 && H / 32 == 1) break;
+              const int cc = c + u;
+              if (l >= 1) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  v[u][j] = __float_as_uint(__uint_as_float(v[u][j]) + p.hbias[(l - 1) & 1][cc * 32 + j]);
               }
-            }
-            if (PREC == PREC_BF16) {
-              uint32_t pk[16];
+              if (PREC == PREC_BF16) {
+                uint32_t pk[16];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) pk[j] = relu_bf16x2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-              tmem_st16(acol + c * 16, pk);
-            } else {
-              uint32_t hv[32];
+                for (int j = 0; j < 16; ++j)
+                  pk[j] = relu_bf16x2(__uint_as_float(v[u][2 * j]), __uint_as_float(v[u][2 * j + 1]));
+                tmem_st16(acol + cc * 16, pk);
+              } else {
+                uint32_t hv[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                float x = fmaxf(__uint_as_float(v[j]), 0.0f);
-                hv[j] = to_tf32(x);
-                if (PREC == PREC_FP32) v[j] = to_tf32(x - __uint_as_float(hv[j]));
+                for (int j = 0; j < 32; ++j) {
+                  const float x = fmaxf(__uint_as_float(v[u][j]), 0.0f);
+                  hv[j] = to_tf32(x);
+                  if (PREC == PREC_FP32) v[u][j] = to_tf32(x - __uint_as_float(hv[j]));
+                }
+                tmem_st32(acol + cc * 32, hv);
+                if (PREC == PREC_FP32) tmem_st32(acol + H + cc * 32, v[u]);
               }
-              tmem_st32(acol + c * 32, hv);
-              if (PREC == PREC_FP32) tmem_st32(acol + H + c * 32, v);
             }
           }
           tmem_wait_st();
@@ -442,33 +469,40 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars[1 + s]);
         } else {
-          // a7: FP32 final layer, relu(x + b) = max(x, -b) + b folded into c_out
-          float acc0 = 0.0f, acc1 = 0.0f;
+          // a7: FP32 final layer; relu(x + b) = max(x, -b) + b with sum_j w_j b_j in c_out;
+          // packed FFMA2 over column pairs, 4 independent accumulator pairs
+          uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-          for (int c = 0; c < H / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld32(dcol + c * 32, v);
+          for (int c = 0; c < H / 32; c += 2) {
+            uint32_t v[2][32];
+            tmem_ld32(dcol + c * 32, v[0]);
+            if (H / 32 > 1) tmem_ld32(dcol + (c + 1) * 32, v[1]);
             tmem_wait_ld();
-            const float4* w4 = reinterpret_cast<const float4*>(sw + c * 32);
-            const float4* n4 = reinterpret_cast<const float4*>(snb + c * 32);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 w = w4[j], nb = n4[j];
-              acc0 = fmaf(w.x, fmaxf(__uint_as_float(v[4 * j + 0]), nb.x), acc0);
-              acc1 = fmaf(w.y, fmaxf(__uint_as_float(v[4 * j + 1]), nb.y), acc1);
-              acc0 = fmaf(w.z, fmaxf(__uint_as_float(v[4 * j + 2]), nb.z), acc0);
-              acc1 = fmaf(w.w, fmaxf(__uint_as_float(v[4 * j + 3]), nb.w), acc1);
+            for (int u = 0; u < 2; ++u) {
+              if (u == 1 && H / 32 == 1) break;
+              const int cc = c + u;
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const float x0 = fmaxf(__uint_as_float(v[u][j]), p.fin_nb[cc * 32 + j]);
+                const float x1 = fmaxf(__uint_as_float(v[u][j + 1]), p.fin_nb[cc * 32 + j + 1]);
+                acc[(j >> 1) & 3] = ffma2(pack2(p.fin_w[cc * 32 + j], p.fin_w[cc * 32 + j + 1]), pack2(x0, x1),
+                                          acc[(j >> 1) & 3]);
+              }
             }
           }
-          t = (acc0 + acc1) + p.c_out;
+          float a8[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) unpack2(acc[j], a8[2 * j], a8[2 * j + 1]);
+          t = (((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]))) + p.c_out;
         }
       }
 
       // ---------------- outputs
       if (mode == MODE_TOPK) {
         const uint32_t key = f2key(t);
-        // conservative filter on the key alone (a stale or torn read only admits
-        // extra candidates; the merge keeps the exact (key, idx) top-k)
+        // conservative filter on the key alone (a stale read only admits extra
+        // candidates; the merge keeps the exact (key, idx) top-k)
         const bool pass = valid && key <= ts.misc[2];
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, pass);
         if (m) {
@@ -480,7 +514,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
             ncand = 0;
           }
           if (pass) {
-            uint32_t pos = ncand + __popc(m & ((1u << lane) - 1u));
+            const uint32_t pos = ncand + __popc(m & ((1u << lane) - 1u));
             mycand[pos].idx = I;
             mycand[pos].key = key;
             mycand[pos].pad = 0;
@@ -491,11 +525,9 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
       } else if (valid) {
         p.t_dense[I - p.begin] = t;
       }
-      // advance to the slot's next tile
-      I += (uint64_t)p.dTiles * TILE_M;
-      ilo += p.dlo;
-      if (ilo >= p.M_lo) { ilo -= p.M_lo; ++ihi; }
-      ihi += p.dhi;
+      I = In;
+      ilo = nlo;
+      ihi = nhi;
     }
     if (mode == MODE_TOPK && ncand) {
       lock_acquire(ts, lane);

@@ -1,0 +1,59 @@
+"""Multi-GPU sweep: index-range shards + ONE all_gather of the per-rank top-k.
+
+SURVEY §8(a) a1 / a10, §8(e): rank r of W sweeps the contiguous shard
+[lo_r, hi_r) with q = N // W, rem = N % W, lo_r = r q + min(r, rem) (no u64
+overflow of r N); its k best are kept as surr_record rows (idx, key) with
+sentinels padding short shards; one ``all_gather_into_tensor`` over NCCL
+(NVLink / NVSwitch) collects the W * k records on every rank; the merge kernel
+(K2) reduces them to the k best.  Every rank ends with the same, bitwise
+identical result, independent of W (the (t, idx) order is total).
+
+One process per GPU (torchrun); ``torch.distributed`` is plumbing only.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    q, rem = divmod(int(n), int(world))
+    lo = rank * q + min(rank, rem)
+    return lo, lo + q + (1 if rank < rem else 0)
+
+
+def gather_records(recs: torch.Tensor, group=None) -> torch.Tensor:
+    """All ranks' [k, 2] int64 record blocks -> [W * k, 2] in rank order (one collective)."""
+    world = dist.get_world_size(group)
+    out = torch.empty((world * recs.shape[0], recs.shape[1]), dtype=recs.dtype, device=recs.device)
+    dist.all_gather_into_tensor(out, recs.contiguous(), group=group)
+    return out
+
+
+def sweep_distributed(local_sweep, merge, n: int, k: int, group=None):
+    """Generic driver: ``local_sweep(lo, hi, k) -> [k, 2] records`` (sorted, sentinel
+    padded), ``merge(records [W*k, 2], W, k) -> result``.  Returns merge's result."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = shard_range(n, world, rank)
+    recs = local_sweep(lo, hi, k)
+    return merge(gather_records(recs, group), world, k)
+
+
+def sweep(surrogate, value_lists, k: int, group=None):
+    """The product path: K1+K2 on this rank's shard, all_gather, K2 merge.
+    Returns (idx int64 [k], t float32 [k]) on every rank."""
+    import numpy as np
+    n = int(np.prod([len(v) for v in value_lists], dtype=object))
+
+    def local(lo, hi, kk):
+        return surrogate.sweep_records(value_lists, kk, lo, hi)
+
+    def merge(recs, world, kk):
+        idx, t, _ = surrogate.merge_topk(recs, world, kk, kk)
+        return idx, t
+
+    return sweep_distributed(local, merge, n, k, group)
