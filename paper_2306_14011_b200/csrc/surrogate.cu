@@ -1,7 +1,7 @@
 // Host runtime and C ABI of the B200 surrogate sweep (include/surrogate.h).
 //
 // Responsibilities: validate descriptors, compute |S| and
-// the decoder's super-digit magic numbers, build the value lookup table
+// the decoder's super-digit radices and per-tile stride digits, build the value lookup table
 // (StandardScaler applied in double, then rounded to the
 // operand format), fold b_1 / device features / y de-standardisation into the
 // layer parameters, pack the UMMA shared-memory image, own device buffers and
@@ -118,16 +118,25 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 bool mul_ovf(uint64_t a, uint64_t b, uint64_t* out) { return __builtin_mul_overflow(a, b, out); }
 
+// digits (group radix R, group 0 most significant) of delta mod prod(R)
+void stride_digits(const uint32_t* R, uint64_t delta, uint32_t* dD) {
+  for (int g = MAXG - 1; g >= 0; --g) {
+    dD[g] = (uint32_t)(delta % R[g]);
+    delta /= R[g];
+  }
+}
+
 // ------------------------------------------------------------ kernel table
 struct KernelInfo {
   const void* fn;
   int nslot, threads;
+  bool bias_mma;
 };
 
 template <int PREC, int H>
 KernelInfo kinfo() {
   using C = Cfg<PREC, H>;
-  return KernelInfo{(const void*)&sweep_kernel<PREC, H>, C::NSLOT, C::THREADS};
+  return KernelInfo{(const void*)&sweep_kernel<PREC, H>, C::NSLOT, C::THREADS, C::BIAS_MMA};
 }
 
 bool get_kernel(int prec, uint32_t H, KernelInfo* ki) {
@@ -179,34 +188,34 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
   h->card = card;
   if (!force && h->space_valid && radix == h->c_radix && values == h->c_values) return SURR_OK;
 
-  // super digits: group g holds K slots 2g, 2g+1 (params, then the ones slot P)
-  const uint32_t G = (P + 1) / 2;
+  // super digits: group g holds A0 slots 2g, 2g+1 (parameter j in slot j, the
+  // ones slot P carrying b_1, zeros after); R_g = product of its parameters' radices
   const bool bf = h->prec == PREC_BF16;
   const size_t esz = bf ? 4 : 16;
-  std::vector<uint64_t> R(G);
-  std::vector<uint32_t> off(G);
+  KParams& k = h->sp;
   size_t entries = 0;
-  for (uint32_t g = 0; g < G; ++g) {
-    const uint32_t a = 2 * g, b = 2 * g + 1;
-    R[g] = (uint64_t)radix[a] * (b < P ? radix[b] : 1u);
-    off[g] = (uint32_t)entries;
-    entries += R[g];
-  }
-  if (entries * esz > 96 * 1024) return fail(h, SURR_E_UNSUPPORTED, "value table too large (%zu entries)", entries);
   std::vector<uint32_t> voff(P);
   for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
-  auto zval = [&](uint32_t j, uint32_t d) {  // StandardScaler / min-max affine map, double
-    return (values[voff[j] + d] - h->hshift[j]) / h->hscale[j];
+  auto slot_val = [&](uint32_t slot, uint32_t d) -> double {  // StandardScaler / min-max affine map
+    if (slot < P) return (values[voff[slot] + d] - h->hshift[slot]) / h->hscale[slot];
+    return slot == P ? 1.0 : 0.0;
   };
+  for (uint32_t g = 0; g < (uint32_t)MAXG; ++g) {
+    const uint32_t a = 2 * g, b = 2 * g + 1;
+    const uint64_t ra = a < P ? radix[a] : 1u, rb = b < P ? radix[b] : 1u;
+    k.R[g] = (uint32_t)(ra * rb);
+    k.lut_off[g] = (uint32_t)entries;
+    entries += ra * rb;
+  }
+  if (entries * esz > 96 * 1024) return fail(h, SURR_E_UNSUPPORTED, "value table too large (%zu entries)", entries);
   std::vector<uint8_t> lut(align_up(entries * esz, 16), 0);
-  for (uint32_t g = 0; g < G; ++g) {
+  for (uint32_t g = 0; g < (uint32_t)MAXG; ++g) {
     const uint32_t a = 2 * g, b = 2 * g + 1;
     const uint32_t rb = b < P ? radix[b] : 1u;
-    for (uint64_t D = 0; D < R[g]; ++D) {
-      const uint32_t da = (uint32_t)(D / rb), db = (uint32_t)(D % rb);
-      const double za = zval(a, da);
-      const double zb = b < P ? zval(b, db) : (b == P ? 1.0 : 0.0);
-      uint8_t* e = lut.data() + (off[g] + D) * esz;
+    for (uint32_t D = 0; D < k.R[g]; ++D) {
+      const uint32_t da = D / rb, db = D % rb;
+      const double za = slot_val(a, da), zb = slot_val(b, db);
+      uint8_t* e = lut.data() + (k.lut_off[g] + (size_t)D) * esz;
       if (bf) {
         uint32_t w = (uint32_t)bf16_rne((float)za) | ((uint32_t)bf16_rne((float)zb) << 16);
         memcpy(e, &w, 4);
@@ -216,51 +225,6 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
         tf32_split(zb, &w[1], &w[3]);
         memcpy(e, w, 16);
       }
-    }
-  }
-  // constant A0 columns after the groups (ones slot when P is even, zeros)
-  KParams& k = h->sp;
-  memset(k.a0_const, 0, sizeof k.a0_const);
-  for (uint32_t slot = 2 * G; slot < (uint32_t)K0; ++slot) {
-    const float v = slot == P ? 1.0f : 0.0f;
-    if (bf) {
-      uint32_t w = bf16_rne(v);
-      k.a0_const[slot / 2] |= (slot & 1) ? (w << 16) : w;
-    } else {
-      k.a0_const[slot] = tf32_rna(v);
-      k.a0_const[K0 + slot] = 0;
-    }
-  }
-  // decoder split: groups [split, G) from I mod M_lo (M_lo <= 2^31), the rest from I div M_lo
-  uint32_t split = G;
-  uint64_t mlo = 1;
-  while (split > 0 && mlo * R[split - 1] <= (1ull << 31)) { mlo *= R[split - 1]; --split; }
-  if (split == 0 && card + 4096 >= (1ull << 31)) {  // keep every decoded index below 2^31
-    split = 1;
-    mlo = 1;
-    for (uint32_t g = 1; g < G; ++g) mlo *= R[g];
-  }
-  if (split > 0) {
-    if (split == G) return fail(h, SURR_E_RANGE, "a single super digit exceeds 2^31");
-    if ((card / mlo) + 2 >= (1ull << 31)) return fail(h, SURR_E_RANGE, "|S| too large for the two-word decoder");
-  }
-  k.G = G;
-  k.split = split;
-  k.M_lo = split ? (uint32_t)mlo : 0x80000000u;
-  for (uint32_t g = 0; g < (uint32_t)MAXG; ++g) {
-    if (g < G) {
-      const uint64_t d = R[g];
-      uint32_t l = 0;
-      while ((1ull << l) < d) ++l;
-      const unsigned __int128 num = (unsigned __int128)1 << (31 + l);
-      const uint64_t m = (uint64_t)((num + d - 1) / d);
-      if (m > 0xFFFFFFFFull) return fail(h, SURR_E_RANGE, "magic number overflow");
-      k.R[g] = (uint32_t)d;
-      k.magic[g] = (uint32_t)m;
-      k.shft[g] = l;
-      k.lut_off[g] = off[g];
-    } else {
-      k.R[g] = 1; k.magic[g] = 0x80000000u; k.shft[g] = 0; k.lut_off[g] = 0;
     }
   }
   if (lut.size() > h->d_lut_cap) {
@@ -291,13 +255,13 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   KParams p = h->mp;
   const KParams& s = h->sp;
   if (mode != MODE_PREDICT) {
-    p.G = s.G; p.split = s.split; p.M_lo = s.M_lo;
-    memcpy(p.R, s.R, sizeof p.R); memcpy(p.magic, s.magic, sizeof p.magic);
-    memcpy(p.shft, s.shft, sizeof p.shft); memcpy(p.lut_off, s.lut_off, sizeof p.lut_off);
-    memcpy(p.a0_const, s.a0_const, sizeof p.a0_const);
-    p.lut_gmem = s.lut_gmem; p.lut_bytes = s.lut_bytes;
+    memcpy(p.R, s.R, sizeof p.R);
+    memcpy(p.lut_off, s.lut_off, sizeof p.lut_off);
+    p.lut_gmem = s.lut_gmem;
+    p.lut_bytes = s.lut_bytes;
   } else {
-    p.G = 0; p.split = 0; p.M_lo = 0x80000000u; p.lut_bytes = 0;
+    for (int g = 0; g < MAXG; ++g) { p.R[g] = 1; p.lut_off[g] = 0; p.dD[g] = 0; }
+    p.lut_bytes = 0;
   }
   p.begin = begin;
   p.end = end;
@@ -306,9 +270,7 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   uint64_t want = (p.num_tiles + nslot - 1) / nslot;
   L->grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms, want));
   p.dTiles = (uint32_t)(nslot * L->grid);
-  const uint64_t delta = (uint64_t)p.dTiles * TILE_M;
-  if (p.split) { p.dhi = (uint32_t)(delta / p.M_lo); p.dlo = (uint32_t)(delta % p.M_lo); }
-  else { p.dhi = 0; p.dlo = (uint32_t)delta; }
+  if (mode != MODE_PREDICT) stride_digits(p.R, (uint64_t)p.dTiles * TILE_M, p.dD);
   p.k = mode == MODE_TOPK ? k : 1;
   // dynamic shared memory layout
   size_t off = align_up(p.w_bytes, 128);
@@ -318,10 +280,10 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   off += (mode == MODE_TOPK ? 2ull * k * sizeof(surr_record) : 0);
   off = align_up(off, 128);
   p.smem_cand = (uint32_t)off;
-  off += (mode == MODE_TOPK ? (size_t)nslot * 4 * CAND_CAP * sizeof(surr_record) : 0);
+  off += (mode == MODE_TOPK ? (size_t)nslot * 4 * CAND_CAP * sizeof(surr_record) : 0);  // last-sub warps
   off = align_up(off, 128);
   p.smem_misc = (uint32_t)off;
-  off += 256;
+  off += 256 + (size_t)nslot * 4 * TILE_M * sizeof(float);  // + final-layer partials [slot][sub][row]
   L->smem = off;
   if (L->smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "shared memory %zu B exceeds 227 KB", L->smem);
   L->p = p;
@@ -494,10 +456,15 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   }
   const bool bf = prec == PREC_BF16;
   const uint32_t esz = bf ? 2 : 4;
+  KernelInfo ki;
+  if (!get_kernel(prec, H, &ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", H);
+  const bool bias_mma = ki.bias_mma;     // hidden biases as an extra UMMA K block
+  const uint32_t kstep = bf ? 16 : 8;
+  const uint32_t KH = H + (bias_mma ? kstep : 0);  // K extent of a hidden-layer B image
   const bool lo1 = !bf;                  // layer 1 carries a lo part in both TF32 modes
   const bool loh = prec == PREC_FP32;    // hidden layers carry a lo part (3xTF32)
   const size_t b1_bytes = (size_t)H * K0 * esz;
-  const size_t bh_bytes = (size_t)H * H * esz;
+  const size_t bh_bytes = (size_t)H * KH * esz;
   KParams& p = h->mp;
   p = KParams{};
   size_t off = 0;
@@ -508,19 +475,17 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   p.lo_delta_h = (uint32_t)bh_bytes;
   p.stride_bh = (uint32_t)align_up(bh_bytes * (loh ? 2 : 1), 128);
   off += (size_t)(NL - 1) * p.stride_bh;
-  off = align_up(off, 128);
-  p.off_bias = (uint32_t)off; off += (size_t)std::max<uint32_t>(NL >= 2 ? NL - 2 : 0, 1) * H * 4;
-  off = align_up(off, 16);
-  p.off_nb = (uint32_t)off; off += H * 4;
-  p.off_w = (uint32_t)off; off += H * 4;
-  p.w_bytes = (uint32_t)align_up(off, 128);
+  p.w_bytes = (uint32_t)align_up(std::max<size_t>(off, 128), 128);
   std::vector<uint8_t> img(p.w_bytes, 0);
 
-  auto put = [&](size_t base, const double* src, uint32_t K, uint32_t N, bool lo_part, size_t lo_base) {
-    // src is [K][N] (fan_in x fan_out); operand element (n, k)
+  // pack src [K][N] (fan_in x fan_out, plus an optional bias row at k = K_src)
+  auto put = [&](size_t base, const double* src, uint32_t Ksrc, const double* bias, uint32_t K, uint32_t N,
+                 bool lo_part, size_t lo_base) {
     for (uint32_t kk = 0; kk < K; ++kk)
       for (uint32_t n = 0; n < N; ++n) {
-        const double x = src[(size_t)kk * N + n];
+        double x = 0.0;
+        if (kk < Ksrc) x = src[(size_t)kk * N + n];
+        else if (kk == Ksrc && bias) x = bias[n];
         const size_t o = pack_offset(n, kk, K, esz);
         if (bf) {
           uint16_t v = bf16_rne((float)x);
@@ -533,38 +498,32 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
         }
       }
   };
-  put(p.off_b1, B1.data(), K0, H, lo1, p.off_b1lo);
+  put(p.off_b1, B1.data(), K0, nullptr, K0, H, lo1, p.off_b1lo);
   for (uint32_t l = 1; l < NL; ++l) {
     const size_t base = p.off_bh + (size_t)(l - 1) * p.stride_bh;
-    put(base, m->W[l], H, H, loh, base + bh_bytes);
+    put(base, m->W[l], H, bias_mma ? m->b[l] : nullptr, KH, H, loh, base + bh_bytes);
   }
-  float* fb = reinterpret_cast<float*>(&img[p.off_bias]);
-  for (uint32_t l = 1; l + 1 < NL; ++l)  // biases of model layers 2 .. NL-1 (hidden epilogues)
-    for (uint32_t n = 0; n < H; ++n) fb[(size_t)(l - 1) * H + n] = (float)m->b[l][n];
   // final layer: t = y_mean + y_scale (sum_j w_j relu(D_j + b_j) + b_out)
   //            = c' + sum_j w'_j max(D_j, -b_j),  w' = y_scale w,  c' = y_mean + y_scale (b_out + sum w b)
+  // (b_j = 0 here when the bias is already in D: layer 1, or folded into the UMMA)
   const double* Wout = m->W[NL];
   const double bout = m->b[NL][0];
-  const double* bl = NL >= 2 ? m->b[NL - 1] : nullptr;  // layer-1 bias is already in D when NL == 1
-  float* fnb = reinterpret_cast<float*>(&img[p.off_nb]);
-  float* fw = reinterpret_cast<float*>(&img[p.off_w]);
+  const double* bl = (NL >= 2 && !bias_mma) ? m->b[NL - 1] : nullptr;
   double cacc = bout;
   for (uint32_t n = 0; n < H; ++n) {
     const double bj = bl ? bl[n] : 0.0;
-    fnb[n] = (float)(-bj);
-    fw[n] = (float)(m->y_scale * Wout[n]);
+    p.fin_nb[n] = (float)(-bj);
+    p.fin_w[n] = (float)(m->y_scale * Wout[n]);
     cacc += Wout[n] * bj;
   }
   p.c_out = (float)(m->y_mean + m->y_scale * cacc);
-  for (uint32_t n = 0; n < H; ++n) { p.fin_w[n] = fw[n]; p.fin_nb[n] = fnb[n]; }
-  for (uint32_t l = 1; l + 1 < NL; ++l)
-    for (uint32_t n = 0; n < H; ++n) p.hbias[l - 1][n] = (float)m->b[l][n];
+  if (!bias_mma)
+    for (uint32_t l = 1; l + 1 < NL; ++l)
+      for (uint32_t n = 0; n < H; ++n) p.hbias[l - 1][n] = (float)m->b[l][n];
   p.NL = NL;
   p.sbo_b1 = (K0 / (16 / esz)) * 128;
-  p.sbo_bh = (H / (16 / esz)) * 128;
-  const int fmt = bf ? 1 : 2;
-  p.idesc_l1 = make_idesc(fmt, H, TILE_M);
-  p.idesc_h = make_idesc(fmt, H, TILE_M);
+  p.sbo_bh = (KH / (16 / esz)) * 128;
+  p.idesc = make_idesc(bf ? 1 : 2, H, TILE_M);
   p.P = P;
 
   if (img.size() > h->d_w_cap) {
@@ -685,12 +644,13 @@ surr_status surrogate_decode_range(surrogate_t* h, const surr_space* space, uint
   if (n == 0) return SURR_OK;
   DecodeParams dp{};
   const KParams& s = h->sp;
-  dp.G = s.G; dp.split = s.split; dp.M_lo = s.M_lo; dp.P = h->P;
-  memcpy(dp.R, s.R, sizeof dp.R); memcpy(dp.magic, s.magic, sizeof dp.magic); memcpy(dp.shft, s.shft, sizeof dp.shft);
+  memcpy(dp.R, s.R, sizeof dp.R);
   for (uint32_t j = 0; j < h->P; ++j) dp.radix[j] = h->c_radix[j];
+  dp.P = h->P;
   dp.first = first; dp.n = n; dp.out = digits_dev;
   const uint32_t threads = 256;
-  const uint64_t blocks = std::min<uint64_t>((n + threads - 1) / threads, 1u << 20);
+  const uint64_t blocks = std::min<uint64_t>((n + threads - 1) / threads, 512);
+  stride_digits(dp.R, blocks * threads, dp.dD);
   decode_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(dp);
   CU(cudaGetLastError());
   ++h->launches;

@@ -2,23 +2,27 @@
 // top-k (a8) and the list merge (K2) for sm_100a.
 //
 // Per flat config index I:
-//   a2  mixed-radix decode, in registers, on "super digits" (pairs of
-//       parameters, radix R_g = r_{2g} r_{2g+1}) by 32-bit magic division;
-//   a3  normalisation prologue = one shared-memory lookup per super digit of
-//       the pre-normalised, pre-rounded operand pair;
-//   a4  layer-1 UMMA, K0 = 16 (14 params + ones column carrying b_1 + 0);
-//   a5  hidden epilogue: tcgen05.ld D -> (+b) -> ReLU -> BF16x2 / TF32 hi-lo
-//       -> tcgen05.st A (the next layer's A operand lives in TMEM);
+//   a2  mixed-radix decode on "super digits": group g = parameters 2g, 2g+1
+//       (radix R_g = r_2g r_2g+1); each thread keeps the digits of its row in
+//       registers and advances them by the constant per-tile index stride with
+//       a carry-propagating odometer (no division in the loop);
+//   a3  normalisation prologue = one shared-memory lookup per group of the
+//       pre-normalised, pre-rounded operand pair (StandardScaler);
+//   a4  layer-1 UMMA, K0 = 16 (14 params + ones slot carrying b_1 + 0);
+//   a5  hidden epilogue: tcgen05.ld D -> ReLU -> BF16x2 / TF32 hi-lo ->
+//       tcgen05.st A (the next layer's A operand lives in TMEM); hidden-layer
+//       biases ride in the UMMA as an extra K block against a constant ones
+//       block in TMEM when it fits (BIAS_MMA), else are added here;
 //   a6  hidden UMMAs, B = weights resident in shared memory (bulk-copied once);
-//   a7  final H -> 1 layer in FP32 on CUDA cores + de-standardisation;
+//   a7  final H -> 1 layer in FP32 on CUDA cores (packed FFMA2) + de-standardisation;
 //   a8  warp ballot filter against the CTA's k-th best, per-warp candidate
 //       buffer, rank-based merge into the CTA's sorted top-k.
 //
-// CTA roles: warp 0 lane 0 issues every tcgen05.mma (work-conserving: it polls
-// the per-slot "A ready" mbarriers); warpgroups 1..NSLOT each own one TMEM
-// slot (D accumulator + A operand for a 128-row tile) and run decode,
-// epilogues and top-k for that slot's tiles, so NSLOT tiles are in flight and
-// one slot's CUDA-core epilogue overlaps the other slot's MMAs.
+// CTA roles: warp 0 lane 0 issues every tcgen05.mma (blocking waits, round
+// robin over slots); warpgroups 1..NSLOT each own one TMEM slot (D accumulator
+// + A operand for a 128-row tile) and run decode, epilogues and top-k for that
+// slot's tiles, so NSLOT tiles are in flight and one slot's CUDA-core epilogue
+// overlaps the other slot's MMAs.
 #pragma once
 #include <cstdint>
 
@@ -30,8 +34,8 @@ namespace surr {
 enum { PREC_BF16 = 0, PREC_FP32 = 1, PREC_TF32 = 2 };
 enum { MODE_TOPK = 0, MODE_DENSE = 1, MODE_PREDICT = 2 };
 
-constexpr int MAXG = 8;       // super-digit groups (P <= 15 -> ceil(P/2) <= 8)
-constexpr int K0 = 16;        // layer-1 K (P + ones column <= 16)
+constexpr int MAXG = 8;       // super-digit groups = A0 column pairs (K0 / 2)
+constexpr int K0 = 16;        // layer-1 K (P + ones slot <= 16)
 constexpr int TILE_M = 128;   // rows per tile (UMMA M)
 constexpr int CAND_CAP = 64;  // per-warp top-k candidate buffer
 constexpr uint32_t KEY_SENT = 0xFFFFFFFFu;
@@ -40,36 +44,34 @@ constexpr uint64_t IDX_SENT = ~0ull;
 struct KParams {
   // rows
   uint64_t begin, end, num_tiles;
-  uint32_t dTiles;          // tile stride of one slot (= NSLOT * gridDim.x)
-  uint32_t dlo, dhi;        // dTiles * 128 split as dhi * M_lo + dlo
-  // decoder (super digits)
-  uint32_t G, split, M_lo;  // groups [split, G) decode from I mod M_lo, [0, split) from I div M_lo
-  uint32_t R[MAXG], magic[MAXG], shft[MAXG], lut_off[MAXG];
-  uint32_t a0_const[2 * K0];  // constant A0 columns past the LUT groups (bf16: [0, 8); tf32: hi [0,16), lo [16,32))
+  uint32_t dTiles;           // tile stride of one slot (= NSLOT * gridDim.x)
+  // decoder: group g covers A0 slots 2g, 2g+1; groups without parameters have R = 1
+  uint32_t R[MAXG];          // group radix
+  uint32_t dD[MAXG];         // digits of the per-tile index stride dTiles * 128
+  uint32_t lut_off[MAXG];    // first table entry of group g
   const void* lut_gmem;
   uint32_t lut_bytes;
   // predict rows
   const float* x;
   uint32_t P;
-  const double* zshift;     // [P]
-  const double* zscale;     // [P]
+  const double* zshift;      // [P]
+  const double* zscale;      // [P]
   // model
-  uint32_t NL;              // UMMA layers (= number of hidden layers)
+  uint32_t NL;               // UMMA layers (= number of hidden layers)
   const void* w_gmem;
   uint32_t w_bytes;
-  uint32_t off_b1, off_b1lo, off_bh, stride_bh, lo_delta_h, off_bias, off_nb, off_w;
+  uint32_t off_b1, off_b1lo, off_bh, stride_bh, lo_delta_h;
   uint32_t sbo_b1, sbo_bh;
-  uint32_t idesc_l1, idesc_h;
+  uint32_t idesc;
   float c_out;
-  // epilogue constants in the kernel-parameter (constant) bank: used directly
-  // as instruction operands, no shared-memory traffic
-  float fin_w[128];         // y_scale * w_out
-  float fin_nb[128];        // -b of the last hidden layer (0 when it is layer 1)
-  float hbias[2][128];      // biases of model layers 2 .. NL-1 (hidden epilogues)
+  // epilogue constants in the kernel-parameter (constant) bank
+  float fin_w[128];          // y_scale * w_out
+  float fin_nb[128];         // -b of the last hidden layer (0 when folded into the UMMA)
+  float hbias[2][128];       // biases of model layers 2 .. NL-1 (when not folded)
   // outputs
   uint32_t k;
-  surr_record* recs;        // MODE_TOPK: gridDim.x * k records
-  float* t_dense;           // MODE_DENSE / MODE_PREDICT
+  surr_record* recs;         // MODE_TOPK: gridDim.x * k records
+  float* t_dense;            // MODE_DENSE / MODE_PREDICT
   uint32_t smem_lut, smem_lists, smem_cand, smem_misc;  // byte offsets in dynamic smem
 };
 
@@ -78,14 +80,18 @@ struct Cfg {
   static constexpr int A_COLS = PREC == PREC_BF16 ? H / 2 : (PREC == PREC_FP32 ? 2 * H : H);
   static constexpr int SLOT_COLS = H + A_COLS;
   static constexpr int NSLOT = (2 * SLOT_COLS <= 512) ? 2 : 1;
-  static constexpr int NEED = NSLOT * SLOT_COLS;
+  // hidden-layer biases as an extra UMMA K block against a shared ones block
+  static constexpr bool BIAS_MMA = NSLOT * SLOT_COLS + 8 <= 512;
+  static constexpr int ONES_COL = NSLOT * SLOT_COLS;
+  static constexpr int NEED = NSLOT * SLOT_COLS + (BIAS_MMA ? 8 : 0);
   static constexpr int TMEM_COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr int THREADS = 128 * (1 + NSLOT);
   static constexpr int PASSES_H = PREC == PREC_FP32 ? 3 : 1;   // hidden layers
   static constexpr int PASSES_1 = PREC == PREC_BF16 ? 1 : 3;   // layer 1
+  static constexpr int KSTEP = PREC == PREC_BF16 ? 16 : 8;     // K per UMMA
   // A0 lo-part column offset (tf32 modes): fp32 keeps lo next to the hidden lo region
   static constexpr int A0_LO = PREC == PREC_FP32 ? H : K0;
-  static_assert(SLOT_COLS * NSLOT <= 512, "TMEM budget");
+  static_assert(NEED <= 512, "TMEM budget");
 };
 
 // order-preserving float -> uint32 (NaN after +inf)
@@ -114,29 +120,27 @@ __device__ __forceinline__ uint64_t make_bdesc(uint32_t saddr, uint32_t sbo) {
   return d;
 }
 
-// q = floor(n / d) for n < 2^31 with m = ceil(2^(31+l) / d), l = ceil(log2 d):
-// floor(2n * m / 2^32) >> l  (exact: m d - 2^(31+l) <= 2^l).
-__device__ __forceinline__ uint32_t magic_div(uint32_t n, uint32_t m, uint32_t l) {
-  return __umulhi(n + n, m) >> l;
-}
-
-// a2: super digits D_g of I = hi * M_lo + lo (groups [split, G) from lo, the
-// rest from hi), least significant group last; D_0 is clamped so that masked
-// rows past |S| still index inside the table.
-template <class PT>
-__device__ __forceinline__ void decode_groups(const PT& p, uint32_t lo, uint32_t hi, uint32_t (&D)[MAXG]) {
+// ------------------------------------------------------------ a2: decoder
+// Super digits of I (group 0 most significant): one u64 division
+// per group, done once per thread.  Rows past |S| (masked tail) clamp the top
+// digit so every table index stays in range.
+__device__ __forceinline__ void init_digits(const uint32_t* R, uint64_t I, uint32_t (&D)[MAXG]) {
 #pragma unroll
   for (int g = MAXG - 1; g >= 0; --g) {
-    D[g] = 0;
-    if (g < (int)p.G) {
-      const bool fromlo = g >= (int)p.split;
-      const uint32_t n = fromlo ? lo : hi;
-      const uint32_t q = magic_div(n, p.magic[g], p.shft[g]);
-      uint32_t dg = n - q * p.R[g];
-      if (g == 0) dg = min(dg, p.R[0] - 1u);
-      if (fromlo) lo = q; else hi = q;
-      D[g] = dg;
-    }
+    const uint64_t r = R[g];
+    D[g] = (uint32_t)(I % r);
+    I /= r;
+  }
+  if (I) D[0] = R[0] - 1u;
+}
+// D <- digits of (I + stride) mod |S|: add the stride's digits with carries.
+__device__ __forceinline__ void odometer_step(const uint32_t* R, const uint32_t* dD, uint32_t (&D)[MAXG]) {
+  uint32_t carry = 0;
+#pragma unroll
+  for (int g = MAXG - 1; g >= 0; --g) {
+    const uint32_t d = D[g] + dD[g] + carry;
+    carry = d >= R[g] ? 1u : 0u;
+    D[g] = carry ? d - R[g] : d;
   }
 }
 
@@ -220,27 +224,17 @@ struct A0Regs {
   uint32_t hi[K0], lo[K0];
 };
 
+// a3: one table lookup per group (pre-normalised, pre-rounded slot pairs)
 template <int PREC>
-__device__ __forceinline__ void make_a0_sweep(const KParams& p, const uint8_t* slut, uint32_t ilo, uint32_t ihi,
+__device__ __forceinline__ void make_a0_sweep(const KParams& p, const uint8_t* slut, const uint32_t (&D)[MAXG],
                                               A0Regs& a) {
-  uint32_t D[MAXG];
-  decode_groups(p, ilo, ihi, D);
 #pragma unroll
   for (int g = 0; g < MAXG; ++g) {
-    if (g < (int)p.G) {
-      if (PREC == PREC_BF16) {
-        a.hi[g] = reinterpret_cast<const uint32_t*>(slut)[p.lut_off[g] + D[g]];
-      } else {
-        const uint4 e = reinterpret_cast<const uint4*>(slut)[p.lut_off[g] + D[g]];
-        a.hi[2 * g] = e.x; a.hi[2 * g + 1] = e.y; a.lo[2 * g] = e.z; a.lo[2 * g + 1] = e.w;
-      }
+    if (PREC == PREC_BF16) {
+      a.hi[g] = reinterpret_cast<const uint32_t*>(slut)[p.lut_off[g] + D[g]];
     } else {
-      if (PREC == PREC_BF16) {
-        a.hi[g] = p.a0_const[g];
-      } else {
-        a.hi[2 * g] = p.a0_const[2 * g]; a.hi[2 * g + 1] = p.a0_const[2 * g + 1];
-        a.lo[2 * g] = p.a0_const[K0 + 2 * g]; a.lo[2 * g + 1] = p.a0_const[K0 + 2 * g + 1];
-      }
+      const uint4 e = reinterpret_cast<const uint4*>(slut)[p.lut_off[g] + D[g]];
+      a.hi[2 * g] = e.x; a.hi[2 * g + 1] = e.y; a.lo[2 * g] = e.z; a.lo[2 * g + 1] = e.w;
     }
   }
 }
@@ -317,6 +311,18 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (C::BIAS_MMA && warp >= 4 && warp < 8) {
+    // constant ones block (A operand of the bias K step): slot 0 = 1, rest 0
+    uint32_t ones[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ones[j] = 0u;
+    ones[0] = PREC == PREC_BF16 ? 0x00003F80u : 0x3F800000u;
+    tmem_st8(tmem_base + (((warp & 3u) * 32u) << 16) + C::ONES_COL, ones);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     // ================= UMMA issuer (one thread) =================
@@ -334,6 +340,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
         rounds = max(rounds, ntile[s]);
       }
       const uint32_t sb = smem_u32(smem);
+      const uint32_t ones = tmem_base + C::ONES_COL;
       for (uint32_t j = 0; j < rounds; ++j) {
         for (uint32_t l = 0; l < p.NL; ++l) {
 #pragma unroll
@@ -344,25 +351,34 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
             tc_fence_after();
             const uint32_t d = tmem_base + s * C::SLOT_COLS;
             const uint32_t a = d + H;
-            uint32_t bhi, blo, sbo, idesc, steps, alo;
-            bool three;
+            uint32_t bhi, blo, sbo, steps, alo;
+            bool three, bias_step;
             if (l == 0) {
-              bhi = sb + p.off_b1; blo = sb + p.off_b1lo; sbo = p.sbo_b1; idesc = p.idesc_l1;
-              steps = PREC == PREC_BF16 ? K0 / 16 : K0 / 8; three = C::PASSES_1 == 3; alo = a + C::A0_LO;
+              bhi = sb + p.off_b1; blo = sb + p.off_b1lo; sbo = p.sbo_b1;
+              steps = K0 / C::KSTEP; three = C::PASSES_1 == 3; alo = a + C::A0_LO; bias_step = false;
             } else {
               bhi = sb + p.off_bh + (l - 1) * p.stride_bh; blo = bhi + p.lo_delta_h; sbo = p.sbo_bh;
-              idesc = p.idesc_h; steps = PREC == PREC_BF16 ? H / 16 : H / 8; three = C::PASSES_H == 3; alo = a + H;
+              steps = H / C::KSTEP; three = C::PASSES_H == 3; alo = a + H; bias_step = C::BIAS_MMA;
             }
             for (uint32_t kk = 0; kk < steps; ++kk) {
               const uint64_t dh = make_bdesc(bhi + kk * 256u, sbo);
               if (PREC == PREC_BF16) {
-                umma_f16_ts(d, a + kk * 8u, dh, idesc, kk > 0);
+                umma_f16_ts(d, a + kk * 8u, dh, p.idesc, kk > 0);
               } else {
-                umma_tf32_ts(d, a + kk * 8u, dh, idesc, kk > 0);
+                umma_tf32_ts(d, a + kk * 8u, dh, p.idesc, kk > 0);
                 if (three) {
-                  umma_tf32_ts(d, a + kk * 8u, make_bdesc(blo + kk * 256u, sbo), idesc, 1u);
-                  umma_tf32_ts(d, alo + kk * 8u, dh, idesc, 1u);
+                  umma_tf32_ts(d, a + kk * 8u, make_bdesc(blo + kk * 256u, sbo), p.idesc, 1u);
+                  umma_tf32_ts(d, alo + kk * 8u, dh, p.idesc, 1u);
                 }
+              }
+            }
+            if (bias_step) {  // D += ones * [b; 0] (the B image carries one extra K block)
+              const uint64_t dh = make_bdesc(bhi + steps * 256u, sbo);
+              if (PREC == PREC_BF16) {
+                umma_f16_ts(d, ones, dh, p.idesc, 1u);
+              } else {
+                umma_tf32_ts(d, ones, dh, p.idesc, 1u);
+                if (three) umma_tf32_ts(d, ones, make_bdesc(blo + steps * 256u, sbo), p.idesc, 1u);
               }
             }
             umma_commit(&bars[3 + s]);
@@ -384,19 +400,18 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
 
     uint64_t tile = (uint64_t)blockIdx.x * C::NSLOT + s;
     uint64_t I = p.begin + tile * TILE_M + row;
-    uint32_t ilo, ihi;
-    if (p.split) { ihi = (uint32_t)(I / p.M_lo); ilo = (uint32_t)(I % p.M_lo); }
-    else { ihi = 0; ilo = (uint32_t)I; }
     const uint64_t dI = (uint64_t)p.dTiles * TILE_M;
+    uint32_t D[MAXG];
+    if (mode != MODE_PREDICT) init_digits(p.R, I, D);
     uint32_t phd = 0;
     mbar_wait(&bars[0], 0);  // table / weights resident
 
-    // software pipeline: the A0 operand of the NEXT tile is decoded while the
+    // software pipeline: the A0 operand of the NEXT tile is built while the
     // last UMMA layer of the current tile runs
     A0Regs a0;
     if (tile < p.num_tiles) {
       if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, I < p.end ? I : p.begin, a0);
-      else make_a0_sweep<PREC>(p, slut, ilo, ihi, a0);
+      else make_a0_sweep<PREC>(p, slut, D, a0);
     }
     for (; tile < p.num_tiles; tile += p.dTiles) {
       const bool valid = I < p.end;
@@ -412,18 +427,19 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[1 + s]);
 
-      // next tile's row index (and its A0, computed below)
       const uint64_t In = I + dI;
-      uint32_t nlo = ilo + p.dlo, nhi = ihi + p.dhi;
-      if (nlo >= p.M_lo) { nlo -= p.M_lo; ++nhi; }
       const bool has_next = tile + p.dTiles < p.num_tiles;
 
       // ---------------- layers
       float t = 0.0f;
       for (uint32_t l = 0; l < p.NL; ++l) {
         if (l + 1 == p.NL && has_next) {
-          if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
-          else make_a0_sweep<PREC>(p, slut, nlo, nhi, a0);
+          if (mode == MODE_PREDICT) {
+            make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
+          } else {
+            odometer_step(p.R, p.dD, D);
+            make_a0_sweep<PREC>(p, slut, D, a0);
+          }
         }
         mbar_wait(&bars[3 + s], phd);
         phd ^= 1u;
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
             for (int u = 0; u < 2; ++u) {
               if (u == 1 && H / 32 == 1) break;
               const int cc = c + u;
-              if (l >= 1) {
+              if (!C::BIAS_MMA && l >= 1) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
                   v[u][j] = __float_as_uint(__uint_as_float(v[u][j]) + p.hbias[(l - 1) & 1][cc * 32 + j]);
@@ -469,8 +485,8 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars[1 + s]);
         } else {
-          // a7: FP32 final layer; relu(x + b) = max(x, -b) + b with sum_j w_j b_j in c_out;
-          // packed FFMA2 over column pairs, 4 independent accumulator pairs
+          // a7: FP32 final layer, packed FFMA2 over column pairs, 4 accumulator pairs;
+          // ReLU threshold 0 when the bias is in D, else relu(x + b) = max(x, -b) + b
           uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
           for (int c = 0; c < H / 32; c += 2) {
@@ -484,8 +500,10 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
               const int cc = c + u;
 #pragma unroll
               for (int j = 0; j < 32; j += 2) {
-                const float x0 = fmaxf(__uint_as_float(v[u][j]), p.fin_nb[cc * 32 + j]);
-                const float x1 = fmaxf(__uint_as_float(v[u][j + 1]), p.fin_nb[cc * 32 + j + 1]);
+                const float th0 = C::BIAS_MMA ? 0.0f : p.fin_nb[cc * 32 + j];
+                const float th1 = C::BIAS_MMA ? 0.0f : p.fin_nb[cc * 32 + j + 1];
+                const float x0 = fmaxf(__uint_as_float(v[u][j]), th0);
+                const float x1 = fmaxf(__uint_as_float(v[u][j + 1]), th1);
                 acc[(j >> 1) & 3] = ffma2(pack2(p.fin_w[cc * 32 + j], p.fin_w[cc * 32 + j + 1]), pack2(x0, x1),
                                           acc[(j >> 1) & 3]);
               }
@@ -526,8 +544,6 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
         p.t_dense[I - p.begin] = t;
       }
       I = In;
-      ilo = nlo;
-      ihi = nhi;
     }
     if (mode == MODE_TOPK && ncand) {
       lock_acquire(ts, lane);
@@ -591,28 +607,29 @@ __global__ void __launch_bounds__(1024, 1)
 }
 
 // ------------------------------------------------------------ decode hook
+// The kernels' decoder on arbitrary ranges: each thread initialises its digits
+// once and then advances by the grid stride with the same odometer.
 struct DecodeParams {
-  uint32_t G, split, M_lo, P;
-  uint32_t R[MAXG], magic[MAXG], shft[MAXG];
+  uint32_t R[MAXG], dD[MAXG];   // group radices, digits of the grid stride
   uint32_t radix[32];
+  uint32_t P;
   uint64_t first, n;
   uint8_t* out;
 };
 
 __global__ void decode_kernel(const __grid_constant__ DecodeParams p) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t I = p.first + i;
-    uint32_t lo, hi;
-    if (p.split) { hi = (uint32_t)(I / p.M_lo); lo = (uint32_t)(I % p.M_lo); }
-    else { hi = 0; lo = (uint32_t)I; }
-    uint32_t D[MAXG];
-    decode_groups(p, lo, hi, D);
-    for (uint32_t g = 0; g < p.G; ++g) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t D[MAXG];
+  init_digits(p.R, p.first + i, D);
+  for (; i < p.n; i += stride) {
+    for (uint32_t g = 0; 2 * g < p.P; ++g) {
       const uint32_t a = 2 * g, b = 2 * g + 1;
       const uint32_t rb = b < p.P ? p.radix[b] : 1u;
       p.out[i * p.P + a] = (uint8_t)(D[g] / rb);
       if (b < p.P) p.out[i * p.P + b] = (uint8_t)(D[g] % rb);
     }
+    odometer_step(p.R, p.dD, D);
   }
 }
 
