@@ -324,11 +324,13 @@ surr_status ensure_recs(surrogate* h, size_t n) {
 
 surr_status launch_merge(surrogate* h, const surr_record* in, uint32_t lists, uint32_t k_in, uint32_t k,
                          uint64_t* oi, float* ot, surr_record* orec, cudaStream_t st) {
-  const size_t smem = (2ull * k + k_in) * sizeof(surr_record);
+  const size_t budget = 200 * 1024 - 2ull * k * sizeof(surr_record);
+  uint32_t chunk = (uint32_t)std::max<size_t>(1, budget / (2ull * k_in * sizeof(surr_record)));
+  chunk = std::min<uint32_t>(chunk, std::max<uint32_t>(lists, 1));
+  const size_t smem = (2ull * k + 2ull * chunk * k_in) * sizeof(surr_record);
   if (smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "merge needs %zu B shared memory", smem);
   CU(cudaFuncSetAttribute((const void*)merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  uint32_t threads = std::min<uint32_t>(1024u, (std::max(k, k_in) + 31) / 32 * 32);
-  merge_kernel<<<1, threads, smem, st>>>(in, lists, k_in, k, oi, ot, orec);
+  merge_kernel<<<1, 1024, smem, st>>>(in, lists, k_in, k, chunk, oi, ot, orec);
   CU(cudaGetLastError());
   ++h->launches;
   return SURR_OK;

@@ -161,6 +161,16 @@ __device__ __forceinline__ uint32_t lower_bound_recs(const surr_record* a, uint3
   return lo;
 }
 
+__device__ __forceinline__ uint32_t upper_bound_recs_fwd(const surr_record* a, uint32_t n, uint32_t key, uint64_t idx) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const surr_record r = a[mid];
+    if (!rec_less(key, idx, r.key, r.idx)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 // Merge the warp's cnt candidates into the CTA list (caller holds the lock).
 __device__ void warp_merge(TopkShared& ts, surr_record* cand, uint32_t cnt, uint32_t k, uint32_t lane) {
   // 1. sort candidates by rank (all keys distinct: idx unique)
@@ -189,7 +199,7 @@ __device__ void warp_merge(TopkShared& ts, surr_record* cand, uint32_t cnt, uint
   }
   for (uint32_t j = lane; j < cnt; j += 32) {
     surr_record c = cand[j];
-    uint32_t p = j + lower_bound_recs(L, k, c.key, c.idx);
+    uint32_t p = j + upper_bound_recs_fwd(L, k, c.key, c.idx);
     if (p < k) O[p] = c;
   }
   __syncwarp();
@@ -567,39 +577,85 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
 }
 
 // ------------------------------------------------------------------ K2
-// Merge `lists` sorted lists of k_in records into the k best (one CTA).
+// Merge `lists` sorted lists of k_in records into the k best (one CTA):
+// lists are loaded a chunk at a time (coalesced, all threads), reduced by a
+// pairwise tree of rank merges in shared memory, then merged into the result.
+// Ties (only sentinels can tie) are broken by list order: elements of the
+// left list use count(right < e), of the right list count(left <= f), so the
+// output positions are a permutation.
+__device__ __forceinline__ uint32_t upper_bound_recs(const surr_record* a, uint32_t n, uint32_t key, uint64_t idx) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const surr_record r = a[mid];
+    if (!rec_less(key, idx, r.key, r.idx)) lo = mid + 1; else hi = mid;  // r <= (key, idx)
+  }
+  return lo;
+}
+
+// out[0..min(na+nb, cap)) = first elements of merge(A[0..na), B[0..nb))
+__device__ __forceinline__ void rank_merge(const surr_record* A, uint32_t na, const surr_record* B, uint32_t nb,
+                                           surr_record* out, uint32_t cap, uint32_t t, uint32_t nt) {
+  for (uint32_t i = t; i < na; i += nt) {
+    const surr_record e = A[i];
+    const uint32_t pp = i + lower_bound_recs(B, nb, e.key, e.idx);
+    if (pp < cap) out[pp] = e;
+  }
+  for (uint32_t i = t; i < nb; i += nt) {
+    const surr_record f = B[i];
+    const uint32_t pp = i + upper_bound_recs(A, na, f.key, f.idx);
+    if (pp < cap) out[pp] = f;
+  }
+}
+
 __global__ void __launch_bounds__(1024, 1)
-    merge_kernel(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k,
+    merge_kernel(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k, uint32_t chunk,
                  uint64_t* out_idx, float* out_t, surr_record* out_recs) {
   extern __shared__ __align__(16) uint8_t sm[];
-  surr_record* T = reinterpret_cast<surr_record*>(sm);
-  surr_record* N = T + k;
-  surr_record* In = N + k;
-  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) { T[i].idx = IDX_SENT; T[i].key = KEY_SENT; T[i].pad = 0; }
-  __syncthreads();
-  for (uint32_t j = 0; j < lists; ++j) {
-    const surr_record* src = in + (size_t)j * k_in;
-    for (uint32_t i = threadIdx.x; i < k_in; i += blockDim.x) In[i] = src[i];
+  surr_record* T = reinterpret_cast<surr_record*>(sm);  // [k] result so far
+  surr_record* T2 = T + k;                              // [k]
+  surr_record* X = T2 + k;                              // [chunk * k_in]
+  surr_record* Y = X + (size_t)chunk * k_in;            // [chunk * k_in]
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  for (uint32_t i = t; i < k; i += nt) { T[i].idx = IDX_SENT; T[i].key = KEY_SENT; T[i].pad = 0; }
+  for (uint32_t c0 = 0; c0 < lists; c0 += chunk) {
+    const uint32_t m = min(chunk, lists - c0);
+    const uint32_t tot = m * k_in;
+    const uint4* src = reinterpret_cast<const uint4*>(in + (size_t)c0 * k_in);
+    for (uint32_t i = t; i < tot; i += nt) reinterpret_cast<uint4*>(X)[i] = src[i];
     __syncthreads();
-    const surr_record worst = T[k - 1];
-    if (rec_less(In[0].key, In[0].idx, worst.key, worst.idx)) {
-      for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-        surr_record e = T[i];
-        uint32_t pp = i + lower_bound_recs(In, k_in, e.key, e.idx);
-        if (pp < k) N[pp] = e;
+    // pairwise tree: nl lists of length len (stride st) -> ceil(nl/2) lists of length min(2 len, k)
+    uint32_t nl = m, len = k_in, st = k_in;
+    surr_record *cur = X, *nxt = Y;
+    while (nl > 1) {
+      const uint32_t nlen = min(2 * len, k);
+      const uint32_t pairs = nl / 2;
+      // threads split across pairs
+      const uint32_t tpp = max(1u, nt / pairs);
+      const uint32_t pr = t / tpp, tt = t % tpp;
+      for (uint32_t pi = pr; pi < pairs; pi += max(1u, nt / tpp)) {
+        rank_merge(cur + (size_t)(2 * pi) * st, len, cur + (size_t)(2 * pi + 1) * st, len, nxt + (size_t)pi * st,
+                   nlen, tt, tpp);
       }
-      for (uint32_t i = threadIdx.x; i < k_in; i += blockDim.x) {
-        surr_record c = In[i];
-        uint32_t pp = i + lower_bound_recs(T, k, c.key, c.idx);
-        if (pp < k) N[pp] = c;
+      if (nl & 1) {
+        for (uint32_t i = t; i < len; i += nt) nxt[(size_t)pairs * st + i] = cur[(size_t)(nl - 1) * st + i];
+        for (uint32_t i = len + t; i < nlen; i += nt) {
+          nxt[(size_t)pairs * st + i].idx = IDX_SENT; nxt[(size_t)pairs * st + i].key = KEY_SENT;
+          nxt[(size_t)pairs * st + i].pad = 0;
+        }
       }
       __syncthreads();
-      surr_record* tmp = T; T = N; N = tmp;
+      surr_record* tmp = cur; cur = nxt; nxt = tmp;
+      nl = (nl + 1) / 2;
+      len = nlen;
     }
+    // merge the chunk's best (cur[0..len)) into T
+    rank_merge(T, k, cur, min(len, k), T2, k, t, nt);
     __syncthreads();
+    surr_record* tmp = T; T = T2; T2 = tmp;
   }
-  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-    surr_record e = T[i];
+  for (uint32_t i = t; i < k; i += nt) {
+    const surr_record e = T[i];
     if (out_idx) out_idx[i] = e.idx;
     if (out_t) out_t[i] = key2f(e.key);
     if (out_recs) out_recs[i] = e;
