@@ -167,6 +167,11 @@ surr_status surrogate_space_size(const surr_space *space, uint64_t *out);
 surr_status surrogate_kernel_timing(surrogate_t *h, int enable);
 surr_status surrogate_kernel_timing_get(surrogate_t *h, double *total_ms, uint32_t *launches);
 
+/* Debug hook: record a clock64 timeline of CTA 0's pipeline events into
+ * trace_dev[n] (device, caller-owned) on subsequent sweeps; NULL disables.
+ * Layout: (round * 4 + slot) * 16 + event (see sweep_kernel3.cuh). */
+surr_status surrogate_debug_trace(surrogate_t *h, unsigned long long *trace_dev, uint32_t n);
+
 /* Bytes of the value lookup table of the cached space (the per-sweep H2D of
  * surrogate_sweep_host). */
 uint32_t surrogate_table_bytes(const surrogate_t *h);

@@ -23,7 +23,7 @@ EXPORTS = [
     "surrogate_predict", "surrogate_sweep", "surrogate_sweep_host", "surrogate_eval_range",
     "surrogate_merge_topk", "surrogate_sweep_records", "surrogate_decode_range", "surrogate_space_size",
     "surrogate_kernel_timing", "surrogate_kernel_timing_get", "surrogate_last_launches",
-    "surrogate_selftest_umma", "surrogate_table_bytes",
+    "surrogate_selftest_umma", "surrogate_table_bytes", "surrogate_debug_trace",
 ]
 
 
@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
         L.surrogate_last_launches.argtypes = [vp]
         L.surrogate_last_launches.restype = u32
         L.surrogate_selftest_umma.argtypes = [i32, i32, u32, u32, vp, vp, vp]
+        L.surrogate_debug_trace.argtypes = [vp, vp, u32]
         L.surrogate_table_bytes.argtypes = [vp]
         L.surrogate_table_bytes.restype = u32
         for name in EXPORTS:
@@ -265,6 +266,11 @@ class Surrogate:
         _check(lib().surrogate_decode_range(self.h, ctypes.byref(d.c), first, n, ctypes.c_void_p(out.data_ptr()),
                                             _stream_ptr(stream)), self.h)
         return out
+
+    def debug_trace(self, buf):
+        """Record CTA 0's pipeline timeline into a device int64 tensor (None: off)."""
+        _check(lib().surrogate_debug_trace(self.h, ctypes.c_void_p(buf.data_ptr()) if buf is not None else None,
+                                           0 if buf is None else buf.numel()), self.h)
 
     def kernel_timing(self, enable: bool):
         _check(lib().surrogate_kernel_timing(self.h, 1 if enable else 0), self.h)

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "sweep_kernel.cuh"
+#include "sweep_kernel3.cuh"
 
 using namespace surr;
 
@@ -52,6 +53,9 @@ struct surrogate {
   surr_record* d_merged = nullptr;
   uint64_t* d_idx = nullptr;
   float* d_t = nullptr;
+  // debug timeline
+  unsigned long long* trace = nullptr;
+  uint32_t trace_n = 0;
   // timing
   bool timing = false;
   std::vector<cudaEvent_t> ev;
@@ -139,7 +143,19 @@ KernelInfo kinfo() {
   return KernelInfo{(const void*)&sweep_kernel<PREC, H>, C::NSLOT, C::THREADS, C::BIAS_MMA};
 }
 
-bool get_kernel(int prec, uint32_t H, KernelInfo* ki) {
+template <int H>
+KernelInfo kinfo3() {
+  using C = Cfg3<H>;
+  return KernelInfo{(const void*)&sweep_kernel3<H>, C::NSLOT, C::THREADS, true};
+}
+
+bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki) {
+  // BF16 nets with at most one hidden->hidden layer: three tiles in flight
+  if (prec == PREC_BF16 && NL <= 2) {
+    if (H == 32) { *ki = kinfo3<32>(); return true; }
+    if (H == 64) { *ki = kinfo3<64>(); return true; }
+    if (H == 128) { *ki = kinfo3<128>(); return true; }
+  }
 #define CASE(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo<P_, H_>(); return true; }
   CASE(PREC_BF16, 32) CASE(PREC_BF16, 64) CASE(PREC_BF16, 128)
@@ -251,7 +267,7 @@ struct Launch {
 };
 
 surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L) {
-  if (!get_kernel(h->prec, h->H, &L->ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
+  if (!get_kernel(h->prec, h->H, h->NL, &L->ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
   KParams p = h->mp;
   const KParams& s = h->sp;
   if (mode != MODE_PREDICT) {
@@ -358,6 +374,8 @@ surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint
   rc = ensure_recs(h, (size_t)L.grid * k);
   if (rc) return rc;
   L.p.recs = h->d_recs;
+  L.p.trace = h->trace;
+  L.p.trace_n = h->trace_n;
   rc = launch(h, L, MODE_TOPK, st);
   if (rc) return rc;
   return launch_merge(h, h->d_recs, (uint32_t)L.grid, k, k, idx_dev, t_dev, recs_dev, st);
@@ -459,7 +477,7 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   const bool bf = prec == PREC_BF16;
   const uint32_t esz = bf ? 2 : 4;
   KernelInfo ki;
-  if (!get_kernel(prec, H, &ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", H);
+  if (!get_kernel(prec, H, L - 1, &ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", H);
   const bool bias_mma = ki.bias_mma;     // hidden biases as an extra UMMA K block
   const uint32_t kstep = bf ? 16 : 8;
   const uint32_t KH = H + (bias_mma ? kstep : 0);  // K extent of a hidden-layer B image
@@ -656,6 +674,13 @@ surr_status surrogate_decode_range(surrogate_t* h, const surr_space* space, uint
   decode_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(dp);
   CU(cudaGetLastError());
   ++h->launches;
+  return SURR_OK;
+}
+
+surr_status surrogate_debug_trace(surrogate_t* h, unsigned long long* trace_dev, uint32_t n) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  h->trace = trace_dev;
+  h->trace_n = trace_dev ? n : 0;
   return SURR_OK;
 }
 

@@ -73,7 +73,18 @@ struct KParams {
   surr_record* recs;         // MODE_TOPK: gridDim.x * k records
   float* t_dense;            // MODE_DENSE / MODE_PREDICT
   uint32_t smem_lut, smem_lists, smem_cand, smem_misc;  // byte offsets in dynamic smem
+  // debug timeline (CTA 0 only): trace[ev] = clock64 of event ev, or null
+  unsigned long long* trace;
+  uint32_t trace_n;
 };
+
+// debug timeline of CTA 0: slot s, tile round j, event e -> one clock64 stamp
+__device__ __forceinline__ void trace_ev(const KParams& p, uint32_t s, uint32_t j, uint32_t e) {
+  if (p.trace && blockIdx.x == 0) {
+    const uint32_t i = (j * 4 + s) * 16 + e;
+    if (i < p.trace_n) p.trace[i] = clock64();
+  }
+}
 
 template <int PREC, int H>
 struct Cfg {
@@ -335,64 +346,77 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
   tc_fence_after();
 
   if (warp == 0) {
-    // ================= UMMA issuer (one thread) =================
-    // Round-robin over slots, layer by layer; every wait is a blocking
-    // (HW-suspending) try_wait so the issuer takes no issue slots from the
-    // epilogue warps sharing its SM sub-partition.
-    if (lane == 0) {
-      mbar_wait(&bars[0], 0);  // weights resident
-      uint32_t ntile[C::NSLOT], ph[C::NSLOT];
-      uint32_t rounds = 0;
-      for (int s = 0; s < C::NSLOT; ++s) {
-        const uint64_t t0 = (uint64_t)blockIdx.x * C::NSLOT + s;
-        ntile[s] = t0 < p.num_tiles ? (uint32_t)((p.num_tiles - t0 - 1) / p.dTiles + 1) : 0u;
-        ph[s] = 0;
-        rounds = max(rounds, ntile[s]);
-      }
-      const uint32_t sb = smem_u32(smem);
-      const uint32_t ones = tmem_base + C::ONES_COL;
-      for (uint32_t j = 0; j < rounds; ++j) {
-        for (uint32_t l = 0; l < p.NL; ++l) {
+    // ================= UMMA issuer (warp 0, converged) =================
+    // Round-robin over slots, layer by layer; waits are blocking (HW-suspending)
+    // try_waits.  The whole warp runs the loop so descriptor arithmetic stays
+    // warp-uniform; one elected lane issues each layer's fully unrolled UMMA
+    // chain (issue cost ~ a few cycles per UMMA instead of ~40 in divergent code).
+    mbar_wait(&bars[0], 0);  // weights resident
+    uint32_t ntile[C::NSLOT], ph[C::NSLOT];
+    uint32_t rounds = 0;
 #pragma unroll
-          for (int s = 0; s < C::NSLOT; ++s) {
-            if (j >= ntile[s]) continue;
-            mbar_wait(&bars[1 + s], ph[s]);
-            ph[s] ^= 1u;
-            tc_fence_after();
-            const uint32_t d = tmem_base + s * C::SLOT_COLS;
-            const uint32_t a = d + H;
-            uint32_t bhi, blo, sbo, steps, alo;
-            bool three, bias_step;
+    for (int s = 0; s < C::NSLOT; ++s) {
+      const uint64_t t0 = (uint64_t)blockIdx.x * C::NSLOT + s;
+      ntile[s] = t0 < p.num_tiles ? (uint32_t)((p.num_tiles - t0 - 1) / p.dTiles + 1) : 0u;
+      ph[s] = 0;
+      rounds = max(rounds, ntile[s]);
+    }
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t ones = tmem_base + C::ONES_COL;
+    const uint64_t d_b1 = make_bdesc(sb + p.off_b1, p.sbo_b1);
+    const uint64_t d_b1lo = make_bdesc(sb + p.off_b1lo, p.sbo_b1);
+    const uint32_t idesc = p.idesc;
+    for (uint32_t j = 0; j < rounds; ++j) {
+      for (uint32_t l = 0; l < p.NL; ++l) {
+        const uint64_t d_bh = make_bdesc(sb + p.off_bh + (l ? l - 1 : 0) * p.stride_bh, p.sbo_bh);
+        const uint64_t d_bhlo = make_bdesc(sb + p.off_bh + (l ? l - 1 : 0) * p.stride_bh + p.lo_delta_h, p.sbo_bh);
+#pragma unroll
+        for (int s = 0; s < C::NSLOT; ++s) {
+          if (j >= ntile[s]) continue;
+          mbar_wait(&bars[1 + s], ph[s]);
+          ph[s] ^= 1u;
+          tc_fence_after();
+          const uint32_t d = tmem_base + s * C::SLOT_COLS;
+          const uint32_t a = d + H;
+          if (elect_one()) {
             if (l == 0) {
-              bhi = sb + p.off_b1; blo = sb + p.off_b1lo; sbo = p.sbo_b1;
-              steps = K0 / C::KSTEP; three = C::PASSES_1 == 3; alo = a + C::A0_LO; bias_step = false;
-            } else {
-              bhi = sb + p.off_bh + (l - 1) * p.stride_bh; blo = bhi + p.lo_delta_h; sbo = p.sbo_bh;
-              steps = H / C::KSTEP; three = C::PASSES_H == 3; alo = a + H; bias_step = C::BIAS_MMA;
-            }
-            for (uint32_t kk = 0; kk < steps; ++kk) {
-              const uint64_t dh = make_bdesc(bhi + kk * 256u, sbo);
-              if (PREC == PREC_BF16) {
-                umma_f16_ts(d, a + kk * 8u, dh, p.idesc, kk > 0);
-              } else {
-                umma_tf32_ts(d, a + kk * 8u, dh, p.idesc, kk > 0);
-                if (three) {
-                  umma_tf32_ts(d, a + kk * 8u, make_bdesc(blo + kk * 256u, sbo), p.idesc, 1u);
-                  umma_tf32_ts(d, alo + kk * 8u, dh, p.idesc, 1u);
+              // K0 = 16: one bf16 step, or two tf32 steps x 3 passes
+#pragma unroll
+              for (int kk = 0; kk < K0 / C::KSTEP; ++kk) {
+                if (PREC == PREC_BF16) {
+                  umma_f16_ts(d, a + kk * 8, d_b1 + kk * 16, idesc, kk > 0);
+                } else {
+                  umma_tf32_ts(d, a + kk * 8, d_b1 + kk * 16, idesc, kk > 0);
+                  umma_tf32_ts(d, a + kk * 8, d_b1lo + kk * 16, idesc, 1u);
+                  umma_tf32_ts(d, a + C::A0_LO + kk * 8, d_b1 + kk * 16, idesc, 1u);
                 }
               }
-            }
-            if (bias_step) {  // D += ones * [b; 0] (the B image carries one extra K block)
-              const uint64_t dh = make_bdesc(bhi + steps * 256u, sbo);
-              if (PREC == PREC_BF16) {
-                umma_f16_ts(d, ones, dh, p.idesc, 1u);
-              } else {
-                umma_tf32_ts(d, ones, dh, p.idesc, 1u);
-                if (three) umma_tf32_ts(d, ones, make_bdesc(blo + steps * 256u, sbo), p.idesc, 1u);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < H / C::KSTEP; ++kk) {
+                if (PREC == PREC_BF16) {
+                  umma_f16_ts(d, a + kk * 8, d_bh + kk * 16, idesc, kk > 0);
+                } else {
+                  umma_tf32_ts(d, a + kk * 8, d_bh + kk * 16, idesc, kk > 0);
+                  if (C::PASSES_H == 3) {
+                    umma_tf32_ts(d, a + kk * 8, d_bhlo + kk * 16, idesc, 1u);
+                    umma_tf32_ts(d, a + H + kk * 8, d_bh + kk * 16, idesc, 1u);
+                  }
+                }
+              }
+              if (C::BIAS_MMA) {  // D += ones * [b; 0] (the B image carries one extra K block)
+                constexpr int kb = H / C::KSTEP;
+                if (PREC == PREC_BF16) {
+                  umma_f16_ts(d, ones, d_bh + kb * 16, idesc, 1u);
+                } else {
+                  umma_tf32_ts(d, ones, d_bh + kb * 16, idesc, 1u);
+                  if (C::PASSES_H == 3) umma_tf32_ts(d, ones, d_bhlo + kb * 16, idesc, 1u);
+                }
               }
             }
             umma_commit(&bars[3 + s]);
           }
+          __syncwarp();
         }
       }
     }

@@ -1,0 +1,183 @@
+// Microbenchmark (development aid): tcgen05.mma issue/execution rate for the
+// shapes K1 uses, and the commit -> mbarrier -> waiting-warp handoff latency.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o umma_rate scripts/umma_rate.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include "../paper_2306_14011_b200/csrc/sm100_ptx.cuh"
+
+using namespace surr;
+
+__device__ __forceinline__ uint64_t bdesc(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((128u >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  return d;
+}
+__host__ __device__ uint32_t idesc_bf16(uint32_t N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+// mode 0: back-to-back UMMAs (N, K=16 each), commit every `batch`, wait, repeat
+// mode 1: ping-pong: thread 0 issues 1 UMMA + commit, warp 4 waits D, arrives A, thread 0 waits A
+__global__ void __launch_bounds__(256, 1) bench(int mode, uint32_t N, int iters, int batch, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[2];
+  __shared__ uint32_t tslot;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) { mbar_init(&bars[0], 1); mbar_init(&bars[1], 1); fence_mbar_init(); }
+    __syncwarp();
+    tmem_alloc<512>(&tslot);
+  }
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3F803F80u;
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t base = tslot;
+  const uint32_t sbo = (128 / 8) * 128;
+  const uint32_t sb = smem_u32(smem);
+  unsigned long long t0 = 0, t1 = 0;
+  if (mode == 0 || mode == 2 || mode == 3) {
+    if (threadIdx.x == 0) {
+      uint32_t ph = 0;
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        for (int b = 0; b < batch; ++b) {
+          if (mode == 0)
+            umma_f16_ts(base, base + 256 + (b & 7) * 8, bdesc(sb + (b & 7) * 256, sbo), idesc_bf16(N), b > 0);
+          else if (mode == 2)  // SS: A (128 x 16) from smem at +40 KB
+            umma_f16_ss(base, bdesc(sb + 40960 + (b & 7) * 256, sbo), bdesc(sb + (b & 7) * 256, sbo),
+                        idesc_bf16(N), b > 0);
+          else  // tf32 TS, K = 8 per instruction
+            umma_tf32_ts(base, base + 256 + (b & 7) * 8, bdesc(sb + (b & 7) * 256, sbo),
+                         (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((128u >> 4) << 24), b > 0);
+        }
+        umma_commit(&bars[0]);
+        mbar_wait(&bars[0], ph);
+        ph ^= 1;
+      }
+      t1 = clock64();
+      out[blockIdx.x * 2] = t1 - t0;
+      out[blockIdx.x * 2 + 1] = (unsigned long long)iters * batch;
+    }
+  } else if (mode == 5 || mode == 6) {
+    // unrolled issue of 8 UMMAs per commit from a converged warp (elected lane);
+    // issuer = warp 0 (mode 5) or warp 7 (mode 6); warps 1..6 burn ALU meanwhile
+    const uint32_t iw = mode == 5 ? 0u : 7u;
+    const uint32_t idesc = idesc_bf16(N);
+    const uint64_t b0 = bdesc(sb, sbo);
+    if (warp == iw) {
+      uint32_t ph = 0;
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        if (elect_one()) {
+#pragma unroll
+          for (int b = 0; b < 8; ++b) umma_f16_ts(base, base + 256 + b * 8, b0 + (uint64_t)(b * 16), idesc, b > 0);
+          umma_commit(&bars[0]);
+        }
+        __syncwarp();
+        mbar_wait(&bars[0], ph);
+        ph ^= 1;
+      }
+      t1 = clock64();
+      if (lane == 0) {
+        out[blockIdx.x * 2] = t1 - t0;
+        out[blockIdx.x * 2 + 1] = (unsigned long long)iters * 8;
+      }
+      if (lane == 0) atomicExch((unsigned*)&tslot + 0, tslot);  // no-op touch
+    } else if (batch > 0) {
+      float x = (float)threadIdx.x;
+      for (int i = 0; i < iters * 200; ++i) x = fmaf(x, 1.0001f, 0.5f);
+      if (x == 0.0f) out[0] = 1;
+    }
+  } else if (mode == 4) {
+    // converged warp 0, elected issue (N, K=16 TS), commit every `batch`
+    if (warp == 0) {
+      uint32_t ph = 0;
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+#pragma unroll 1
+        for (int b = 0; b < batch; ++b) {
+          const uint64_t bd = bdesc(sb + (b & 7) * 256, sbo);
+          if (elect_one()) umma_f16_ts(base, base + 256 + (b & 7) * 8, bd, idesc_bf16(N), b > 0);
+          __syncwarp();
+        }
+        if (elect_one()) umma_commit(&bars[0]);
+        __syncwarp();
+        mbar_wait(&bars[0], ph);
+        ph ^= 1;
+      }
+      t1 = clock64();
+      if (lane == 0) {
+        out[blockIdx.x * 2] = t1 - t0;
+        out[blockIdx.x * 2 + 1] = (unsigned long long)iters * batch;
+      }
+    }
+  } else {
+    // ping-pong latency: MMA thread <-> epilogue warp 4
+    if (threadIdx.x == 0) {
+      uint32_t ph = 0;
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        umma_f16_ts(base, base + 256, bdesc(sb, sbo), idesc_bf16(N), 0);
+        umma_commit(&bars[0]);
+        mbar_wait(&bars[1], ph);
+        tc_fence_after();
+        ph ^= 1;
+      }
+      t1 = clock64();
+      out[blockIdx.x * 2] = t1 - t0;
+      out[blockIdx.x * 2 + 1] = iters;
+    } else if (warp == 4) {
+      uint32_t ph = 0;
+      for (int it = 0; it < iters; ++it) {
+        mbar_wait(&bars[0], ph);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(base + (0u << 16), v);  // touch D like an epilogue
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[1]);
+        ph ^= 1;
+        if (v[0] == 12345u) out[0] = 0;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(base, 512); }
+}
+
+int main() {
+  unsigned long long* d;
+  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  cudaMalloc(&d, 148 * 2 * 8);
+  std::vector<unsigned long long> h(148 * 2);
+  struct C { int mode; uint32_t N; int iters, batch; const char* what; };
+  C cs[] = {{5, 128, 200, 0, "unrolled x8, issuer warp0, idle others"}, {5, 64, 200, 0, "  same N=64"},
+            {5, 128, 200, 1, "unrolled x8, issuer warp0, busy others"}, {6, 128, 200, 1, "unrolled x8, issuer warp7, busy others"},
+            {6, 64, 200, 1, "  same N=64 warp7 busy"}, {6, 256, 200, 1, "  same N=256 warp7 busy"},{4, 128, 50, 64, "elected N=128 x64"}, {4, 64, 50, 64, "elected N=64 x64"},
+            {4, 256, 50, 64, "elected N=256 x64"}, {4, 128, 200, 9, "elected N=128 x9 per commit"},{2, 128, 50, 64, "SS N=128 x64"}, {2, 64, 50, 64, "SS N=64 x64"}, {2, 256, 50, 64, "SS N=256 x64"},
+            {3, 128, 50, 64, "TF32 TS N=128 K=8 x64"}, {3, 256, 50, 64, "TF32 TS N=256 x64"},{0, 128, 200, 8, "N=128 K=16 x8 per commit"},  {0, 64, 200, 8, "N=64 x8"},
+            {0, 128, 50, 64, "N=128 x64"},                {0, 64, 50, 64, "N=64 x64"},
+            {0, 256, 50, 64, "N=256 x64"},                {0, 128, 400, 1, "N=128 x1 (issue+commit+wait)"},
+            {1, 128, 400, 1, "ping-pong MMA->warp->MMA, N=128"}, {1, 64, 400, 1, "ping-pong N=64"}};
+  for (int rep = 0; rep < 2; ++rep)
+  for (auto& c : cs) {
+    for (int grid : {148}) {
+      bench<<<grid, 256, 80 * 1024>>>(c.mode, c.N, c.iters, c.batch, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+      cudaMemcpy(h.data(), d, grid * 2 * 8, cudaMemcpyDeviceToHost);
+      double cyc = 0;
+      for (int b = 0; b < grid; ++b) cyc += (double)h[b * 2] / h[b * 2 + 1];
+      printf("%-40s grid %3d: %8.1f cycles per %s\n", c.what, grid, cyc / grid, c.mode == 0 ? "UMMA" : "round trip");
+    }
+  }
+  return 0;
+}
