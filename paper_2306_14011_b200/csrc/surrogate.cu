@@ -47,6 +47,7 @@ struct surrogate {
   size_t d_lut_cap = 0;
   KParams sp{};  // space part (decoder) of the kernel parameters
   uint64_t card = 0;
+  uint32_t spg = 2;  // parameter slots per decoder group of the cached table
   // buffers
   surr_record* d_recs = nullptr;
   size_t d_recs_cap = 0;
@@ -143,18 +144,22 @@ KernelInfo kinfo() {
   return KernelInfo{(const void*)&sweep_kernel<PREC, H>, C::NSLOT, C::THREADS, C::BIAS_MMA};
 }
 
-template <int H>
+template <int H, int SPG>
 KernelInfo kinfo3() {
   using C = Cfg3<H>;
-  return KernelInfo{(const void*)&sweep_kernel3<H>, C::NSLOT, C::THREADS, true};
+  return KernelInfo{(const void*)&sweep_kernel3<H, SPG>, C::NSLOT, C::THREADS, true};
 }
 
-bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki) {
+bool uses_kernel3(int prec, uint32_t H, uint32_t NL) {
+  return prec == PREC_BF16 && NL <= 2 && (H == 32 || H == 64 || H == 128);
+}
+
+bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg = 2) {
   // BF16 nets with at most one hidden->hidden layer: three tiles in flight
-  if (prec == PREC_BF16 && NL <= 2) {
-    if (H == 32) { *ki = kinfo3<32>(); return true; }
-    if (H == 64) { *ki = kinfo3<64>(); return true; }
-    if (H == 128) { *ki = kinfo3<128>(); return true; }
+  if (uses_kernel3(prec, H, NL)) {
+    if (H == 32) { *ki = spg == 4 ? kinfo3<32, 4>() : kinfo3<32, 2>(); return true; }
+    if (H == 64) { *ki = spg == 4 ? kinfo3<64, 4>() : kinfo3<64, 2>(); return true; }
+    if (H == 128) { *ki = spg == 4 ? kinfo3<128, 4>() : kinfo3<128, 2>(); return true; }
   }
 #define CASE(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo<P_, H_>(); return true; }
@@ -204,41 +209,62 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
   h->card = card;
   if (!force && h->space_valid && radix == h->c_radix && values == h->c_values) return SURR_OK;
 
-  // super digits: group g holds A0 slots 2g, 2g+1 (parameter j in slot j, the
-  // ones slot P carrying b_1, zeros after); R_g = product of its parameters' radices
+  // super digits: group g holds A0 slots [spg g, spg (g+1)) (parameter j in slot j,
+  // the ones slot P carrying b_1, zeros after); R_g = product of its parameters'
+  // radices.  spg = 4 (8-byte entries = two packed bf16 columns) for the 3-slot
+  // BF16 kernel when the table fits in 64 KB, else 2.
   const bool bf = h->prec == PREC_BF16;
-  const size_t esz = bf ? 4 : 16;
   KParams& k = h->sp;
-  size_t entries = 0;
   std::vector<uint32_t> voff(P);
   for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
   auto slot_val = [&](uint32_t slot, uint32_t d) -> double {  // StandardScaler / min-max affine map
     if (slot < P) return (values[voff[slot] + d] - h->hshift[slot]) / h->hscale[slot];
     return slot == P ? 1.0 : 0.0;
   };
+  auto table_entries = [&](uint32_t spg_) {
+    uint64_t e = 0;
+    for (uint32_t g = 0; g < (uint32_t)K0 / spg_; ++g) {
+      uint64_t r = 1;
+      for (uint32_t q = 0; q < spg_; ++q) r *= (spg_ * g + q) < P ? radix[spg_ * g + q] : 1u;
+      e += r;
+    }
+    return e;
+  };
+  uint32_t spg = 2;
+  if (uses_kernel3(h->prec, h->H, h->NL) && table_entries(4) * 8 <= 64 * 1024) spg = 4;
+  const uint32_t ng = K0 / spg;
+  const size_t esz = bf ? 2 * spg : 16;  // bf16: spg packed halves; tf32 (spg 2): hi pair + lo pair
+  size_t entries = 0;
   for (uint32_t g = 0; g < (uint32_t)MAXG; ++g) {
-    const uint32_t a = 2 * g, b = 2 * g + 1;
-    const uint64_t ra = a < P ? radix[a] : 1u, rb = b < P ? radix[b] : 1u;
-    k.R[g] = (uint32_t)(ra * rb);
+    uint64_t r = 1;
+    if (g < ng)
+      for (uint32_t q = 0; q < spg; ++q) r *= (spg * g + q) < P ? radix[spg * g + q] : 1u;
+    k.R[g] = (uint32_t)r;
     k.lut_off[g] = (uint32_t)entries;
-    entries += ra * rb;
+    entries += g < ng ? r : 0;
   }
   if (entries * esz > 96 * 1024) return fail(h, SURR_E_UNSUPPORTED, "value table too large (%zu entries)", entries);
   std::vector<uint8_t> lut(align_up(entries * esz, 16), 0);
-  for (uint32_t g = 0; g < (uint32_t)MAXG; ++g) {
-    const uint32_t a = 2 * g, b = 2 * g + 1;
-    const uint32_t rb = b < P ? radix[b] : 1u;
+  for (uint32_t g = 0; g < ng; ++g) {
     for (uint32_t D = 0; D < k.R[g]; ++D) {
-      const uint32_t da = D / rb, db = D % rb;
-      const double za = slot_val(a, da), zb = slot_val(b, db);
+      // digits of the group's slots, first slot most significant
+      uint32_t dig[4] = {0, 0, 0, 0}, rem = D;
+      for (int q = (int)spg - 1; q >= 0; --q) {
+        const uint32_t slot = spg * g + q;
+        const uint32_t r = slot < P ? radix[slot] : 1u;
+        dig[q] = rem % r;
+        rem /= r;
+      }
       uint8_t* e = lut.data() + (k.lut_off[g] + (size_t)D) * esz;
       if (bf) {
-        uint32_t w = (uint32_t)bf16_rne((float)za) | ((uint32_t)bf16_rne((float)zb) << 16);
-        memcpy(e, &w, 4);
+        for (uint32_t q = 0; q < spg; ++q) {
+          const uint16_t v = bf16_rne((float)slot_val(spg * g + q, dig[q]));
+          memcpy(e + 2 * q, &v, 2);
+        }
       } else {
         uint32_t w[4];
-        tf32_split(za, &w[0], &w[2]);
-        tf32_split(zb, &w[1], &w[3]);
+        tf32_split(slot_val(2 * g, dig[0]), &w[0], &w[2]);
+        tf32_split(slot_val(2 * g + 1, dig[1]), &w[1], &w[3]);
         memcpy(e, w, 16);
       }
     }
@@ -255,6 +281,7 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
   h->lut.swap(lut);
   h->c_radix = radix;
   h->c_values = values;
+  h->spg = spg;
   h->space_valid = true;
   return SURR_OK;
 }
@@ -267,7 +294,7 @@ struct Launch {
 };
 
 surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L) {
-  if (!get_kernel(h->prec, h->H, h->NL, &L->ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
+  if (!get_kernel(h->prec, h->H, h->NL, &L->ki, h->spg)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
   KParams p = h->mp;
   const KParams& s = h->sp;
   if (mode != MODE_PREDICT) {
@@ -533,7 +560,8 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   for (uint32_t n = 0; n < H; ++n) {
     const double bj = bl ? bl[n] : 0.0;
     p.fin_nb[n] = (float)(-bj);
-    p.fin_w[n] = (float)(m->y_scale * Wout[n]);
+    // kernels with the bias in the UMMA evaluate w relu(x) as (w/2) x + (w/2) |x|
+    p.fin_w[n] = (float)(m->y_scale * Wout[n] * (bias_mma ? 0.5 : 1.0));
     cacc += Wout[n] * bj;
   }
   p.c_out = (float)(m->y_mean + m->y_scale * cacc);
@@ -667,6 +695,7 @@ surr_status surrogate_decode_range(surrogate_t* h, const surr_space* space, uint
   memcpy(dp.R, s.R, sizeof dp.R);
   for (uint32_t j = 0; j < h->P; ++j) dp.radix[j] = h->c_radix[j];
   dp.P = h->P;
+  dp.spg = h->spg;
   dp.first = first; dp.n = n; dp.out = digits_dev;
   const uint32_t threads = 256;
   const uint64_t blocks = std::min<uint64_t>((n + threads - 1) / threads, 512);

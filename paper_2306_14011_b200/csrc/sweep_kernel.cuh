@@ -79,11 +79,14 @@ struct KParams {
 };
 
 // debug timeline of CTA 0: slot s, tile round j, event e -> one clock64 stamp
+// (compiled in only with -DSURR_TRACE)
 __device__ __forceinline__ void trace_ev(const KParams& p, uint32_t s, uint32_t j, uint32_t e) {
+#ifdef SURR_TRACE
   if (p.trace && blockIdx.x == 0) {
     const uint32_t i = (j * 4 + s) * 16 + e;
     if (i < p.trace_n) p.trace[i] = clock64();
   }
+#endif
 }
 
 template <int PREC, int H>
@@ -143,6 +146,26 @@ __device__ __forceinline__ void init_digits(const uint32_t* R, uint64_t I, uint3
     I /= r;
   }
   if (I) D[0] = R[0] - 1u;
+}
+template <int NG>
+__device__ __forceinline__ void init_digits_n(const uint32_t* R, uint64_t I, uint32_t (&D)[MAXG]) {
+#pragma unroll
+  for (int g = NG - 1; g >= 0; --g) {
+    const uint64_t r = R[g];
+    D[g] = (uint32_t)(I % r);
+    I /= r;
+  }
+  if (I) D[0] = R[0] - 1u;
+}
+template <int NG>
+__device__ __forceinline__ void odometer_step_n(const uint32_t* R, const uint32_t* dD, uint32_t (&D)[MAXG]) {
+  uint32_t carry = 0;
+#pragma unroll
+  for (int g = NG - 1; g >= 0; --g) {
+    const uint32_t d = D[g] + dD[g] + carry;
+    carry = d >= R[g] ? 1u : 0u;
+    D[g] = carry ? d - R[g] : d;
+  }
 }
 // D <- digits of (I + stride) mod |S|: add the stride's digits with carries.
 __device__ __forceinline__ void odometer_step(const uint32_t* R, const uint32_t* dD, uint32_t (&D)[MAXG]) {
@@ -257,6 +280,17 @@ __device__ __forceinline__ void make_a0_sweep(const KParams& p, const uint8_t* s
       const uint4 e = reinterpret_cast<const uint4*>(slut)[p.lut_off[g] + D[g]];
       a.hi[2 * g] = e.x; a.hi[2 * g + 1] = e.y; a.lo[2 * g] = e.z; a.lo[2 * g + 1] = e.w;
     }
+  }
+}
+
+// 4-slot groups (bf16): one 8-byte table entry = two packed A0 columns
+__device__ __forceinline__ void make_a0_sweep4(const KParams& p, const uint8_t* slut, const uint32_t (&D)[MAXG],
+                                               A0Regs& a) {
+#pragma unroll
+  for (int g = 0; g < K0 / 4; ++g) {
+    const uint2 e = reinterpret_cast<const uint2*>(slut)[p.lut_off[g] + D[g]];
+    a.hi[2 * g] = e.x;
+    a.hi[2 * g + 1] = e.y;
   }
 }
 
@@ -534,12 +568,18 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
               const int cc = c + u;
 #pragma unroll
               for (int j = 0; j < 32; j += 2) {
-                const float th0 = C::BIAS_MMA ? 0.0f : p.fin_nb[cc * 32 + j];
-                const float th1 = C::BIAS_MMA ? 0.0f : p.fin_nb[cc * 32 + j + 1];
-                const float x0 = fmaxf(__uint_as_float(v[u][j]), th0);
-                const float x1 = fmaxf(__uint_as_float(v[u][j + 1]), th1);
-                acc[(j >> 1) & 3] = ffma2(pack2(p.fin_w[cc * 32 + j], p.fin_w[cc * 32 + j + 1]), pack2(x0, x1),
-                                          acc[(j >> 1) & 3]);
+                const uint64_t w2 = pack2(p.fin_w[cc * 32 + j], p.fin_w[cc * 32 + j + 1]);
+                if (C::BIAS_MMA) {
+                  // w relu(x) = (w/2) x + (w/2) |x|  (fin_w holds w/2; |x| is a free FFMA2 operand modifier)
+                  const uint64_t x2 = pack2(__uint_as_float(v[u][j]), __uint_as_float(v[u][j + 1]));
+                  const uint64_t a2 = pack2(fabsf(__uint_as_float(v[u][j])), fabsf(__uint_as_float(v[u][j + 1])));
+                  acc[(j >> 1) & 1] = ffma2(w2, x2, acc[(j >> 1) & 1]);
+                  acc[2 + ((j >> 1) & 1)] = ffma2(w2, a2, acc[2 + ((j >> 1) & 1)]);
+                } else {
+                  const float x0 = fmaxf(__uint_as_float(v[u][j]), p.fin_nb[cc * 32 + j]);
+                  const float x1 = fmaxf(__uint_as_float(v[u][j + 1]), p.fin_nb[cc * 32 + j + 1]);
+                  acc[(j >> 1) & 3] = ffma2(w2, pack2(x0, x1), acc[(j >> 1) & 3]);
+                }
               }
             }
           }
@@ -692,7 +732,7 @@ __global__ void __launch_bounds__(1024, 1)
 struct DecodeParams {
   uint32_t R[MAXG], dD[MAXG];   // group radices, digits of the grid stride
   uint32_t radix[32];
-  uint32_t P;
+  uint32_t P, spg;              // parameters; parameter slots per group
   uint64_t first, n;
   uint8_t* out;
 };
@@ -703,11 +743,14 @@ __global__ void decode_kernel(const __grid_constant__ DecodeParams p) {
   uint32_t D[MAXG];
   init_digits(p.R, p.first + i, D);
   for (; i < p.n; i += stride) {
-    for (uint32_t g = 0; 2 * g < p.P; ++g) {
-      const uint32_t a = 2 * g, b = 2 * g + 1;
-      const uint32_t rb = b < p.P ? p.radix[b] : 1u;
-      p.out[i * p.P + a] = (uint8_t)(D[g] / rb);
-      if (b < p.P) p.out[i * p.P + b] = (uint8_t)(D[g] % rb);
+    for (uint32_t g = 0; p.spg * g < p.P; ++g) {
+      uint32_t rem = D[g];
+      for (int q = (int)p.spg - 1; q >= 0; --q) {
+        const uint32_t slot = p.spg * g + q;
+        const uint32_t r = slot < p.P ? p.radix[slot] : 1u;
+        if (slot < p.P) p.out[i * p.P + slot] = (uint8_t)(rem % r);
+        rem /= r;
+      }
     }
     odometer_step(p.R, p.dD, D);
   }

@@ -65,6 +65,15 @@ __device__ __forceinline__ void topk_offer(TopkShared& ts, surr_record* mycand, 
   }
 }
 
+// acc += w relu(x) for a column pair, as (w/2) x + (w/2) |x|: two FFMA2, |x| is
+// a free operand modifier (fin_w holds y_scale * w / 2)
+__device__ __forceinline__ void relu_dot2(const KParams& p, uint32_t v0, uint32_t v1, int n, uint64_t (&acc)[4], int j) {
+  const uint64_t w2 = pack2(p.fin_w[n], p.fin_w[n + 1]);
+  const float x0 = __uint_as_float(v0), x1 = __uint_as_float(v1);
+  acc[(j >> 1) & 1] = ffma2(w2, pack2(x0, x1), acc[(j >> 1) & 1]);
+  acc[2 + ((j >> 1) & 1)] = ffma2(w2, pack2(fabsf(x0), fabsf(x1)), acc[2 + ((j >> 1) & 1)]);
+}
+
 // FP32 partial of the final layer over NC columns starting at TMEM column
 // `col`, output neurons starting at n0 (bias already in D: ReLU threshold 0)
 template <int NC>
@@ -75,11 +84,7 @@ __device__ __forceinline__ float final_partial(const KParams& p, uint32_t col, i
     tmem_ld16(col, v);
     tmem_wait_ld();
 #pragma unroll
-    for (int j = 0; j < 16; j += 2) {
-      const float x0 = fmaxf(__uint_as_float(v[j]), 0.0f);
-      const float x1 = fmaxf(__uint_as_float(v[j + 1]), 0.0f);
-      acc[(j >> 1) & 3] = ffma2(pack2(p.fin_w[n0 + j], p.fin_w[n0 + j + 1]), pack2(x0, x1), acc[(j >> 1) & 3]);
-    }
+    for (int j = 0; j < 16; j += 2) relu_dot2(p, v[j], v[j + 1], n0 + j, acc, j);
   }
 #pragma unroll
   for (int c = 0; c < NC / 32; c += 2) {
@@ -92,11 +97,7 @@ __device__ __forceinline__ float final_partial(const KParams& p, uint32_t col, i
       if (u == 1 && NC / 32 == 1) break;
       const int base = n0 + (c + u) * 32;
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float x0 = fmaxf(__uint_as_float(v[u][j]), 0.0f);
-        const float x1 = fmaxf(__uint_as_float(v[u][j + 1]), 0.0f);
-        acc[(j >> 1) & 3] = ffma2(pack2(p.fin_w[base + j], p.fin_w[base + j + 1]), pack2(x0, x1), acc[(j >> 1) & 3]);
-      }
+      for (int j = 0; j < 32; j += 2) relu_dot2(p, v[u][j], v[u][j + 1], base + j, acc, j);
     }
   }
   float a8[8];
@@ -121,20 +122,19 @@ template <int NC>
 __device__ __forceinline__ float final_compute(const KParams& p, const uint32_t (&v)[64], int n0) {
   uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-  for (int j = 0; j < NC; j += 2) {
-    const float x0 = fmaxf(__uint_as_float(v[j]), 0.0f);
-    const float x1 = fmaxf(__uint_as_float(v[j + 1]), 0.0f);
-    acc[(j >> 1) & 3] = ffma2(pack2(p.fin_w[n0 + j], p.fin_w[n0 + j + 1]), pack2(x0, x1), acc[(j >> 1) & 3]);
-  }
+  for (int j = 0; j < NC; j += 2) relu_dot2(p, v[j], v[j + 1], n0 + j, acc, j);
   float a8[8];
 #pragma unroll
   for (int j = 0; j < 4; ++j) unpack2(acc[j], a8[2 * j], a8[2 * j + 1]);
   return ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
 }
 
-template <int H>
+template <int H, int SPG>
 __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
     sweep_kernel3(const __grid_constant__ KParams p, int mode) {
+  // SPG = parameter slots per decoder group: 4 (two A0 columns per 8-byte table
+  // entry, 4 odometer digits) when the table fits, else 2 (8 digits)
+  constexpr int NG = K0 / SPG;
   using C = Cfg3<H>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5;
@@ -235,13 +235,14 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
   uint64_t I = p.begin + tile * TILE_M + row;
   const uint64_t dI = (uint64_t)p.dTiles * TILE_M;
   uint32_t D[MAXG];
-  if (mode != MODE_PREDICT) init_digits(p.R, I, D);
+  if (mode != MODE_PREDICT) init_digits_n<NG>(p.R, I, D);
   uint32_t phd = 0;
   mbar_wait(&bars[0], 0);
 
   A0Regs a0;
   if (tile < p.num_tiles) {
     if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, I < p.end ? I : p.begin, a0);
+    else if (SPG == 4) make_a0_sweep4(p, slut, D, a0);
     else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
     tmem_st8(a0col, a0.hi);
     tmem_wait_st();
@@ -263,7 +264,10 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
       t = final_partial<H>(p, dcol, 0);
       if (has_next) {
         if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, In < p.end ? In : p.begin, a0);
-        else { odometer_step(p.R, p.dD, D); make_a0_sweep<PREC_BF16>(p, slut, D, a0); }
+        else {
+          odometer_step_n<NG>(p.R, p.dD, D);
+          if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
+        }
         tmem_st8(a0col, a0.hi);
         tmem_wait_st();
         issue(0);
@@ -306,7 +310,10 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
       // ---- next tile's A0 while L2b runs (its 8-column area is idle now)
       if (has_next) {
         if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, In < p.end ? In : p.begin, a0);
-        else { odometer_step(p.R, p.dD, D); make_a0_sweep<PREC_BF16>(p, slut, D, a0); }
+        else {
+          odometer_step_n<NG>(p.R, p.dD, D);
+          if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
+        }
         tmem_st8(a0col, a0.hi);
       }
       // ---- L2b done -> load the second half, start the next tile's L1, then compute
