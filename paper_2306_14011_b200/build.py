@@ -25,7 +25,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         if all(os.path.getmtime(s) <= t for s in srcs):
             return LIB_PATH
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, os.path.join(PKG, "csrc", "surrogate.cu")]
+    extra = os.environ.get("SURR_EXTRA_FLAGS", "").split()  # e.g. -DSURR_TRACE for the timeline hook
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB_PATH, os.path.join(PKG, "csrc", "surrogate.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stderr[-4000:])

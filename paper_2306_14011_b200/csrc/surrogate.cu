@@ -136,6 +136,7 @@ struct KernelInfo {
   const void* fn;
   int nslot, threads;
   bool bias_mma;
+  bool a0_smem = false;  // SS-form A0 tiles + ones block in shared memory
 };
 
 template <int PREC, int H>
@@ -146,8 +147,11 @@ KernelInfo kinfo() {
 
 template <int H, int SPG>
 KernelInfo kinfo3() {
-  using C = Cfg3<H>;
-  return KernelInfo{(const void*)&sweep_kernel3<H, SPG>, C::NSLOT, C::THREADS, true};
+  constexpr int NS = 4;  // four 128-row tiles in flight per SM
+  using C = Cfg3<H, NS>;
+  KernelInfo ki{(const void*)&sweep_kernel3<H, SPG, NS>, C::NSLOT, C::THREADS, true};
+  ki.a0_smem = C::A0_SMEM;
+  return ki;
 }
 
 bool uses_kernel3(int prec, uint32_t H, uint32_t NL) {
@@ -326,7 +330,12 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   off += (mode == MODE_TOPK ? (size_t)nslot * 4 * CAND_CAP * sizeof(surr_record) : 0);  // last-sub warps
   off = align_up(off, 128);
   p.smem_misc = (uint32_t)off;
-  off += 256 + (size_t)nslot * 4 * TILE_M * sizeof(float);  // + final-layer partials [slot][sub][row]
+  off += 256;
+  off = align_up(off, 1024);
+  p.smem_a0 = (uint32_t)off;
+  off += L->ki.a0_smem ? (size_t)nslot * 4096 : 0;
+  p.smem_ones = (uint32_t)off;
+  off += L->ki.a0_smem ? 4096 : 0;
   L->smem = off;
   if (L->smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "shared memory %zu B exceeds 227 KB", L->smem);
   L->p = p;

@@ -73,6 +73,7 @@ struct KParams {
   surr_record* recs;         // MODE_TOPK: gridDim.x * k records
   float* t_dense;            // MODE_DENSE / MODE_PREDICT
   uint32_t smem_lut, smem_lists, smem_cand, smem_misc;  // byte offsets in dynamic smem
+  uint32_t smem_a0, smem_ones;  // SS-form A0 tiles / ones block (4-slot kernel)
   // debug timeline (CTA 0 only): trace[ev] = clock64 of event ev, or null
   unsigned long long* trace;
   uint32_t trace_n;

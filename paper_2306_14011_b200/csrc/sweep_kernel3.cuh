@@ -26,17 +26,30 @@
 
 namespace surr {
 
-template <int H>
+template <int H, int NS = 3>
 struct Cfg3 {
-  static constexpr int NSLOT = 3;
-  static constexpr int A0_COL = NSLOT * H;           // + 8 * slot
+  static constexpr int NSLOT = NS;
+  // NS = 4: the layer-1 operand A0 and the bias ones block live in shared
+  // memory (SS-form UMMA for those two small steps) so that the four H-column
+  // accumulator regions alone fill TMEM
+  static constexpr bool A0_SMEM = NS * H + NS * 8 + 8 > 512;
+  static constexpr int A0_COL = NSLOT * H;           // + 8 * slot (TMEM variant)
   static constexpr int ONES_COL = NSLOT * H + 8 * NSLOT;
-  static constexpr int NEED = ONES_COL + 8;
+  static constexpr int NEED = A0_SMEM ? NSLOT * H : ONES_COL + 8;
   static constexpr int TMEM_COLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr int THREADS = 128 * NSLOT;
+  static constexpr int A0_TILE_BYTES = 128 * 16 * 2;  // 128 rows x K 16 bf16, K-major core matrices
   static_assert(NEED <= 512, "TMEM budget");
   static_assert(H % 32 == 0 && H <= 128, "H");
 };
+
+// A0 row -> shared-memory operand tile (K-major, no swizzle: 8-row x 16-byte
+// core matrices, K halves 128 B apart (LBO), 8-row groups 256 B apart (SBO))
+__device__ __forceinline__ void st_a0_smem(uint8_t* tile, uint32_t row, const uint32_t* cols8) {
+  uint8_t* base = tile + (row >> 3) * 256 + (row & 7) * 16;
+  *reinterpret_cast<uint4*>(base) = make_uint4(cols8[0], cols8[1], cols8[2], cols8[3]);
+  *reinterpret_cast<uint4*>(base + 128) = make_uint4(cols8[4], cols8[5], cols8[6], cols8[7]);
+}
 
 // a8 for one row: ballot filter, per-warp candidate buffer, merge when full
 __device__ __forceinline__ void topk_offer(TopkShared& ts, surr_record* mycand, uint32_t& ncand, bool valid, float t,
@@ -129,13 +142,13 @@ __device__ __forceinline__ float final_compute(const KParams& p, const uint32_t 
   return ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
 }
 
-template <int H, int SPG>
-__global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
+template <int H, int SPG, int NS>
+__global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     sweep_kernel3(const __grid_constant__ KParams p, int mode) {
   // SPG = parameter slots per decoder group: 4 (two A0 columns per 8-byte table
   // entry, 4 odometer digits) when the table fits, else 2 (8 digits)
   constexpr int NG = K0 / SPG;
-  using C = Cfg3<H>;
+  using C = Cfg3<H, NS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t lane = lane_id();
@@ -181,8 +194,13 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 8; ++j) ones[j] = 0u;
     ones[0] = 0x00003F80u;  // bf16 1.0 in K slot 0
-    tmem_st8(tmem_base + ((warp * 32u) << 16) + C::ONES_COL, ones);
-    tmem_wait_st();
+    if (C::A0_SMEM) {
+      st_a0_smem(smem + p.smem_ones, warp * 32u + lane, ones);
+      fence_proxy_async_smem();
+    } else {
+      tmem_st8(tmem_base + ((warp * 32u) << 16) + C::ONES_COL, ones);
+      tmem_wait_st();
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -196,6 +214,16 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
   const uint32_t dslot = tmem_base + s * H;                 // lane 0 view (UMMA operands)
   const uint32_t dcol = dslot + tl;                          // this warp's lanes
   const uint32_t a0col = tmem_base + tl + C::A0_COL + 8 * s;
+  uint8_t* a0tile = smem + p.smem_a0 + s * C::A0_TILE_BYTES;
+  // A0 of this warp's row -> TMEM (st only; caller waits) or shared memory (+ proxy fence)
+  auto put_a0 = [&](const A0Regs& a) {
+    if (C::A0_SMEM) {
+      st_a0_smem(a0tile, row, a.hi);
+      fence_proxy_async_smem();
+    } else {
+      tmem_st8(a0col, a.hi);
+    }
+  };
   const uint8_t* slut = smem + p.smem_lut;
   surr_record* mycand = ts.cand + (size_t)warp * CAND_CAP;
   uint32_t ncand = 0;
@@ -204,6 +232,8 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
   // UMMA operands (warp-uniform)
   const uint32_t sb = smem_u32(smem);
   const uint32_t ones = tmem_base + C::ONES_COL;
+  const uint64_t d_ones = make_bdesc(sb + p.smem_ones, 256);
+  const uint64_t d_a0 = make_bdesc(sb + p.smem_a0 + s * C::A0_TILE_BYTES, 256);
   const uint32_t idesc_full = p.idesc;
   const uint32_t idesc_half = (p.idesc & ~(0x3Fu << 17)) | (((uint32_t)(H / 2) >> 3) << 17);
   const uint64_t d_b1 = make_bdesc(sb + p.off_b1, p.sbo_b1);
@@ -218,12 +248,14 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
       tc_fence_after();
       if (elect_one()) {
         if (phase == 0) {
-          umma_f16_ts(dslot, tmem_base + C::A0_COL + 8 * s, d_b1, idesc_full, 0u);
+          if (C::A0_SMEM) umma_f16_ss(dslot, d_a0, d_b1, idesc_full, 0u);
+          else umma_f16_ts(dslot, tmem_base + C::A0_COL + 8 * s, d_b1, idesc_full, 0u);
         } else {
           const uint64_t bd = phase == 1 ? d_b2a : d_b2b;
 #pragma unroll
           for (int kk = 0; kk < H / 16; ++kk) umma_f16_ts(dslot + H / 2, dslot + kk * 8, bd + kk * 16, idesc_half, kk > 0);
-          umma_f16_ts(dslot + H / 2, ones, bd + (H / 16) * 16, idesc_half, 1u);
+          if (C::A0_SMEM) umma_f16_ss(dslot + H / 2, d_ones, bd + (H / 16) * 16, idesc_half, 1u);
+          else umma_f16_ts(dslot + H / 2, ones, bd + (H / 16) * 16, idesc_half, 1u);
         }
         umma_commit(&bars[4 + s]);
       }
@@ -244,8 +276,8 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
     if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, I < p.end ? I : p.begin, a0);
     else if (SPG == 4) make_a0_sweep4(p, slut, D, a0);
     else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
-    tmem_st8(a0col, a0.hi);
-    tmem_wait_st();
+    put_a0(a0);
+    if (!C::A0_SMEM) tmem_wait_st();
     issue(0);  // L1 of the first tile
   }
   uint32_t jr = 0;
@@ -268,8 +300,8 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
           odometer_step_n<NG>(p.R, p.dD, D);
           if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
         }
-        tmem_st8(a0col, a0.hi);
-        tmem_wait_st();
+        put_a0(a0);
+        if (!C::A0_SMEM) tmem_wait_st();
         issue(0);
       }
     } else {
@@ -314,7 +346,7 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
           odometer_step_n<NG>(p.R, p.dD, D);
           if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
         }
-        tmem_st8(a0col, a0.hi);
+        put_a0(a0);
       }
       // ---- L2b done -> load the second half, start the next tile's L1, then compute
       mbar_wait(&bars[4 + s], phd);
@@ -323,7 +355,7 @@ __global__ void __launch_bounds__(Cfg3<H>::THREADS, 1)
       if (tr) trace_ev(p, s, jr, 5);
       final_load<H / 2>(dcol + H / 2, v);
       if (has_next) {
-        tmem_wait_st();
+        if (!C::A0_SMEM) tmem_wait_st();
         issue(0);  // next tile's L1: A0 stored and all of D read
       }
       const float pb = final_compute<H / 2>(p, v, H / 2);
