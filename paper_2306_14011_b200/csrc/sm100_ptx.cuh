@@ -180,9 +180,10 @@ __device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
   return d;
 }
+// round to nearest even into tf32 (one F2FP.TF32; cvt.rna costs four SASS ops)
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t d;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(d) : "f"(x));
+  asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(d) : "f"(x));
   return d;
 }
 

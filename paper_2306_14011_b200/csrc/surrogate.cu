@@ -20,6 +20,7 @@
 
 #include "sweep_kernel.cuh"
 #include "sweep_kernel3.cuh"
+#include "sweep_kernel5.cuh"
 
 using namespace surr;
 
@@ -93,15 +94,16 @@ uint16_t bf16_rne(float f) {  // same as __float2bfloat16_rn for finite values
   u += 0x7FFFu + ((u >> 16) & 1u);
   return (uint16_t)(u >> 16);
 }
-uint32_t tf32_rna(float f) {  // same as cvt.rna.tf32.f32 for finite values
+uint32_t tf32_rn(float f) {  // same as cvt.rn.tf32.f32 (nearest even) for finite values
   uint32_t u = f32_bits(f);
   if ((u & 0x7FFFFFFFu) >= 0x7F800000u) return u;
-  return (u + 0x1000u) & 0xFFFFE000u;
+  return (u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
 }
+// hi = tf32(x), lo = fp32(x) - hi exactly (the UMMA reads lo's top 19 bits)
 void tf32_split(double x, uint32_t* hi, uint32_t* lo) {
   float f = (float)x;
-  *hi = tf32_rna(f);
-  *lo = tf32_rna(f - bits_f32(*hi));
+  *hi = tf32_rn(f);
+  *lo = f32_bits(f - bits_f32(*hi));
 }
 
 // K-major, no-swizzle UMMA operand image of an N x K matrix (element (n,k) =
@@ -137,7 +139,16 @@ struct KernelInfo {
   int nslot, threads;
   bool bias_mma;
   bool a0_smem = false;  // SS-form A0 tiles + ones block in shared memory
+  uint32_t red_bytes = 0;  // shared-memory partials of split-column epilogues
 };
+
+template <int PREC, int H>
+KernelInfo kinfo5() {
+  using C = Cfg5<PREC, H>;
+  KernelInfo ki{(const void*)&sweep_kernel5<PREC, H>, C::NSLOT, C::THREADS, false};
+  ki.red_bytes = C::NSLOT * C::NSUB * TILE_M * 4;
+  return ki;
+}
 
 template <int PREC, int H>
 KernelInfo kinfo() {
@@ -164,6 +175,14 @@ bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg 
     if (H == 32) { *ki = spg == 4 ? kinfo3<32, 4>() : kinfo3<32, 2>(); return true; }
     if (H == 64) { *ki = spg == 4 ? kinfo3<64, 4>() : kinfo3<64, 2>(); return true; }
     if (H == 128) { *ki = spg == 4 ? kinfo3<128, 4>() : kinfo3<128, 2>(); return true; }
+  }
+  // TF32-family nets with at most one hidden->hidden layer: self-issuing, split columns
+  if (prec != PREC_BF16 && NL <= 2) {
+#define CASE5(P_, H_) \
+  if (prec == P_ && H == H_) { *ki = kinfo5<P_, H_>(); return true; }
+    CASE5(PREC_FP32, 32) CASE5(PREC_FP32, 64) CASE5(PREC_FP32, 128)
+    CASE5(PREC_TF32, 32) CASE5(PREC_TF32, 64) CASE5(PREC_TF32, 128)
+#undef CASE5
   }
 #define CASE(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo<P_, H_>(); return true; }
@@ -333,7 +352,7 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   off += 256;
   off = align_up(off, 1024);
   p.smem_a0 = (uint32_t)off;
-  off += L->ki.a0_smem ? (size_t)nslot * 4096 : 0;
+  off += std::max<size_t>(L->ki.a0_smem ? (size_t)nslot * 4096 : 0, L->ki.red_bytes);
   p.smem_ones = (uint32_t)off;
   off += L->ki.a0_smem ? 4096 : 0;
   L->smem = off;
@@ -531,6 +550,9 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   p.lo_delta_h = (uint32_t)bh_bytes;
   p.stride_bh = (uint32_t)align_up(bh_bytes * (loh ? 2 : 1), 128);
   off += (size_t)(NL - 1) * p.stride_bh;
+  off = align_up(off, 16);
+  p.off_fin = (uint32_t)off;  // final-layer [w' (H floats), -b (H floats)] for shared-memory readers
+  off += 2ull * H * 4;
   p.w_bytes = (uint32_t)align_up(std::max<size_t>(off, 128), 128);
   std::vector<uint8_t> img(p.w_bytes, 0);
 
@@ -574,6 +596,10 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     cacc += Wout[n] * bj;
   }
   p.c_out = (float)(m->y_mean + m->y_scale * cacc);
+  {
+    float* fwb = reinterpret_cast<float*>(&img[p.off_fin]);
+    for (uint32_t n = 0; n < H; ++n) { fwb[n] = p.fin_w[n]; fwb[H + n] = p.fin_nb[n]; }
+  }
   if (!bias_mma)
     for (uint32_t l = 1; l + 1 < NL; ++l)
       for (uint32_t n = 0; n < H; ++n) p.hbias[l - 1][n] = (float)m->b[l][n];
@@ -762,14 +788,14 @@ surr_status surrogate_selftest_umma(int cuda_device, int precision, uint32_t n, 
       const float x = b_host[(size_t)kk * n + j];
       const size_t o = pack_offset(j, kk, k, esz);
       if (bf) { uint16_t v = bf16_rne(x); memcpy(&img[o], &v, 2); }
-      else { uint32_t v = tf32_rna(x); memcpy(&img[o], &v, 4); }
+      else { uint32_t v = tf32_rn(x); memcpy(&img[o], &v, 4); }
     }
   std::vector<uint32_t> a((size_t)128 * k, 0);  // TMEM image per row: bf16 pairs or tf32 words
   for (uint32_t r = 0; r < 128; ++r)
     for (uint32_t kk = 0; kk < k; ++kk) {
       const float x = a_host[(size_t)r * k + kk];
       if (bf) a[(size_t)r * k + kk / 2] |= (uint32_t)bf16_rne(x) << ((kk & 1) * 16);
-      else a[(size_t)r * k + kk] = tf32_rna(x);
+      else a[(size_t)r * k + kk] = tf32_rn(x);
     }
   void *dA = nullptr, *dB = nullptr, *dD = nullptr;
   CU(cudaMalloc(&dA, a.size() * 4));

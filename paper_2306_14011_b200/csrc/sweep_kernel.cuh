@@ -24,6 +24,7 @@
 // slot's tiles, so NSLOT tiles are in flight and one slot's CUDA-core epilogue
 // overlaps the other slot's MMAs.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 
 #include "sm100_ptx.cuh"
@@ -61,13 +62,14 @@ struct KParams {
   const void* w_gmem;
   uint32_t w_bytes;
   uint32_t off_b1, off_b1lo, off_bh, stride_bh, lo_delta_h;
+  uint32_t off_fin;          // final-layer [w' (H), -b (H)] floats in the shared-memory image
   uint32_t sbo_b1, sbo_bh;
   uint32_t idesc;
   float c_out;
   // epilogue constants in the kernel-parameter (constant) bank
-  float fin_w[128];          // y_scale * w_out
-  float fin_nb[128];         // -b of the last hidden layer (0 when folded into the UMMA)
-  float hbias[2][128];       // biases of model layers 2 .. NL-1 (when not folded)
+  alignas(16) float fin_w[128];  // y_scale * w_out (16-byte aligned: LDCU.128 operand loads)
+  alignas(16) float fin_nb[128];  // -b of the last hidden layer (0 when folded into the UMMA)
+  alignas(16) float hbias[2][128];  // biases of model layers 2 .. NL-1 (when not folded)
   // outputs
   uint32_t k;
   surr_record* recs;         // MODE_TOPK: gridDim.x * k records
@@ -78,6 +80,9 @@ struct KParams {
   unsigned long long* trace;
   uint32_t trace_n;
 };
+
+static_assert(offsetof(KParams, fin_w) % 16 == 0 && offsetof(KParams, fin_nb) % 16 == 0,
+              "epilogue constants must stay 16-byte aligned in the parameter bank (LDCU.128)");
 
 // debug timeline of CTA 0: slot s, tile round j, event e -> one clock64 stamp
 // (compiled in only with -DSURR_TRACE)
@@ -314,7 +319,7 @@ __device__ __forceinline__ void make_a0_predict(const KParams& p, uint64_t r, A0
 #pragma unroll
     for (int j = 0; j < K0; ++j) {
       a.hi[j] = to_tf32(z[j]);
-      a.lo[j] = to_tf32(z[j] - __uint_as_float(a.hi[j]));
+      a.lo[j] = __float_as_uint(z[j] - __uint_as_float(a.hi[j]));  // exact; the UMMA truncates it to tf32
     }
   }
 }
@@ -542,7 +547,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
                 for (int j = 0; j < 32; ++j) {
                   const float x = fmaxf(__uint_as_float(v[u][j]), 0.0f);
                   hv[j] = to_tf32(x);
-                  if (PREC == PREC_FP32) v[u][j] = to_tf32(x - __uint_as_float(hv[j]));
+                  if (PREC == PREC_FP32) v[u][j] = __float_as_uint(x - __uint_as_float(hv[j]));
                 }
                 tmem_st32(acol + cc * 32, hv);
                 if (PREC == PREC_FP32) tmem_st32(acol + H + cc * 32, v[u]);

@@ -1,0 +1,282 @@
+// K1 for the TF32-family precisions (SURR_PREC_FP32 = 3xTF32 hidden layers,
+// SURR_PREC_TF32 = 1xTF32 hidden layers; both with a 3xTF32 first layer),
+// nets with at most one hidden->hidden layer, H <= 128.
+//
+// TMEM per slot: D (H fp32 columns) + A (H columns tf32 hi, + H lo for 3xTF32):
+// FP32 = 3H (one slot at H = 128), TF32 = 2H (two slots).  To shorten the
+// per-tile dependency chain, each slot's columns are split across NSUB
+// warpgroups (TMEM lane quadrant = warp % 4, so a row's columns can be shared
+// by several warps but not its lanes): sub q owns columns [q CPS, (q+1) CPS)
+// of every epilogue and the final-layer partial over the same columns; the
+// partials meet in shared memory and the last sub runs the top-k.  As in the
+// BF16 kernel there is no central MMA warp: after the slot's warps pass a
+// named barrier, one elected lane of the slot's first warp issues the layer's
+// fully unrolled UMMA chain (kind::tf32, A from TMEM) and commits it.
+#pragma once
+#include "sweep_kernel.cuh"
+
+namespace surr {
+
+template <int PREC, int H>
+struct Cfg5 {
+  static constexpr int A_COLS = PREC == PREC_FP32 ? 2 * H : H;
+  static constexpr int SLOT_COLS = H + A_COLS;
+  static constexpr int NSLOT = 512 / SLOT_COLS >= 2 ? 2 : 1;
+  static constexpr int NSUB0 = NSLOT == 2 ? 2 : 4;
+  static constexpr int NSUB = (H / 32 < NSUB0) ? H / 32 : NSUB0;  // warpgroups per slot
+  static constexpr int CPS = H / NSUB;                            // columns per sub (multiple of 32)
+  static constexpr int NEED = NSLOT * SLOT_COLS;
+  static constexpr int TMEM_COLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr int THREADS = 128 * NSLOT * NSUB;
+  static constexpr int THREE_H = PREC == PREC_FP32;  // 3 passes in hidden layers
+  static constexpr int A0_LO = PREC == PREC_FP32 ? H : K0;
+  static_assert(NEED <= 512, "TMEM budget");
+};
+
+template <int PREC, int H>
+__global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
+    sweep_kernel5(const __grid_constant__ KParams p, int mode) {
+  using C = Cfg5<PREC, H>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t lane = lane_id();
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_misc);  // [0] load, [4 + s] d ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.smem_misc + 64);
+  float* red = reinterpret_cast<float*>(smem + p.smem_a0);           // [slot][sub][row] partials
+  TopkShared ts;
+  ts.lists = reinterpret_cast<surr_record*>(smem + p.smem_lists);
+  ts.cand = reinterpret_cast<surr_record*>(smem + p.smem_cand);
+  ts.misc = reinterpret_cast<volatile uint32_t*>(smem + p.smem_misc + 128);
+
+  // ---- setup
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&bars[0], 1);
+      for (int s = 0; s < C::NSLOT; ++s) mbar_init(&bars[4 + s], 1);
+      fence_mbar_init();
+      fence_proxy_async_smem();
+      const uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
+      mbar_arrive_expect_tx(&bars[0], total);
+      for (uint32_t off = 0; off < p.w_bytes; off += 32768u)
+        bulk_g2s(smem + off, (const uint8_t*)p.w_gmem + off, min(32768u, p.w_bytes - off), &bars[0]);
+      if (mode != MODE_PREDICT && p.lut_bytes) bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[0]);
+    }
+    __syncwarp();
+    tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  } else if (warp == 1 && mode == MODE_TOPK) {
+    for (uint32_t i = lane; i < p.k; i += 32) {
+      ts.lists[i].idx = IDX_SENT;
+      ts.lists[i].key = KEY_SENT;
+      ts.lists[i].pad = 0;
+    }
+    if (lane == 0) {
+      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // ---- roles: warpgroup wg = s * NSUB + q
+  const uint32_t wg = warp >> 2;
+  const uint32_t s = wg / C::NSUB;
+  const uint32_t q = wg % C::NSUB;
+  const bool first = q == 0, last = q == C::NSUB - 1;
+  const uint32_t wq = warp & 3u;
+  const uint32_t row = wq * 32u + lane;
+  const uint32_t tl = (wq * 32u) << 16;
+  const uint32_t dslot = tmem_base + s * C::SLOT_COLS;  // lane-0 view (UMMA operands)
+  const uint32_t dcol = dslot + tl + q * C::CPS;         // this warp's D columns
+  const uint32_t acol = dslot + tl + H;                  // this warp's A region
+  const uint8_t* slut = smem + p.smem_lut;
+  surr_record* mycand = ts.cand + (size_t)(s * 4 + wq) * CAND_CAP;
+  uint32_t ncand = 0;
+  const uint32_t bar_id = 1 + s;
+  const bool issuer = first && wq == 0;
+  const uint32_t sb = smem_u32(smem);
+  const uint64_t d_b1 = make_bdesc(sb + p.off_b1, p.sbo_b1);
+  const uint64_t d_b1lo = make_bdesc(sb + p.off_b1lo, p.sbo_b1);
+  const uint64_t d_b2 = make_bdesc(sb + p.off_bh, p.sbo_bh);
+  const uint64_t d_b2lo = make_bdesc(sb + p.off_bh + p.lo_delta_h, p.sbo_bh);
+  const uint32_t idesc = p.idesc;
+
+  auto issue = [&](int layer) {
+    tc_fence_before();
+    named_bar_sync(bar_id, 128 * C::NSUB);
+    if (issuer) {
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a = dslot + H;
+        if (layer == 0) {
+#pragma unroll
+          for (int kk = 0; kk < K0 / 8; ++kk) {
+            umma_tf32_ts(dslot, a + kk * 8, d_b1 + kk * 16, idesc, kk > 0);
+            umma_tf32_ts(dslot, a + kk * 8, d_b1lo + kk * 16, idesc, 1u);
+            umma_tf32_ts(dslot, a + C::A0_LO + kk * 8, d_b1 + kk * 16, idesc, 1u);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < H / 8; ++kk) {
+            umma_tf32_ts(dslot, a + kk * 8, d_b2 + kk * 16, idesc, kk > 0);
+            if (C::THREE_H) {
+              umma_tf32_ts(dslot, a + kk * 8, d_b2lo + kk * 16, idesc, 1u);
+              umma_tf32_ts(dslot, a + H + kk * 8, d_b2 + kk * 16, idesc, 1u);
+            }
+          }
+        }
+        umma_commit(&bars[4 + s]);
+      }
+      __syncwarp();
+    }
+  };
+
+  uint64_t tile = (uint64_t)blockIdx.x * C::NSLOT + s;
+  uint64_t I = p.begin + tile * TILE_M + row;
+  const uint64_t dI = (uint64_t)p.dTiles * TILE_M;
+  uint32_t D[MAXG];
+  if (first && mode != MODE_PREDICT) init_digits(p.R, I, D);
+  uint32_t phd = 0;
+  mbar_wait(&bars[0], 0);
+
+  A0Regs a0;
+  auto put_a0 = [&]() {  // sub 0 stores the layer-1 operand (tf32 hi / lo slots)
+    tmem_st16(acol, a0.hi);
+    tmem_st16(acol + C::A0_LO, a0.lo);
+    tmem_wait_st();
+  };
+  if (first && tile < p.num_tiles) {
+    if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, I < p.end ? I : p.begin, a0);
+    else make_a0_sweep<PREC>(p, slut, D, a0);
+    put_a0();
+  }
+  if (tile < p.num_tiles) issue(0);
+  uint32_t jr = 0;
+  for (; tile < p.num_tiles; tile += p.dTiles, ++jr) {
+    const bool tr = q == 0 && wq == 0 && lane == 0;
+    if (tr) trace_ev(p, s, jr, 0);
+    const bool valid = I < p.end;
+    const uint64_t In = I + dI;
+    const bool has_next = tile + p.dTiles < p.num_tiles;
+    float part = 0.0f;
+    for (uint32_t l = 0; l < p.NL; ++l) {
+      mbar_wait(&bars[4 + s], phd);
+      phd ^= 1u;
+      tc_fence_after();
+      if (tr) trace_ev(p, s, jr, 1 + 2 * l);
+      if (l + 1 < p.NL) {
+        // a5: hidden epilogue over this sub's columns -> A (tf32 hi [, lo])
+#pragma unroll
+        for (int c = 0; c < C::CPS / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(dcol + c * 32, v);
+          tmem_wait_ld();
+          uint32_t hv[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = fmaxf(__uint_as_float(v[j]), 0.0f);  // layer-1 bias rides in A0's ones slot
+            hv[j] = to_tf32(x);
+            if (C::THREE_H) v[j] = __float_as_uint(x - __uint_as_float(hv[j]));  // exact; truncated by the UMMA
+          }
+          tmem_st32(acol + q * C::CPS + c * 32, hv);
+          if (C::THREE_H) tmem_st32(acol + H + q * C::CPS + c * 32, v);
+        }
+        tmem_wait_st();
+        if (tr) trace_ev(p, s, jr, 2);
+        issue(1);
+      } else {
+        // a7: final-layer partial over this sub's columns (relu(x + b) = max(x, -b) + b)
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int c = 0; c < C::CPS / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(dcol + c * 32, v);
+          tmem_wait_ld();
+          // w and -b of this sub's columns: broadcast 16-byte shared-memory loads
+          // (the column offset depends on the warpgroup, so no constant-bank operands)
+          const float4* w4 = reinterpret_cast<const float4*>(smem + p.off_fin) + (q * C::CPS + c * 32) / 4;
+          const float4* nb4 = w4 + H / 4;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 w = w4[j / 4], nb = nb4[j / 4];
+            const float x0 = fmaxf(__uint_as_float(v[j]), nb.x), x1 = fmaxf(__uint_as_float(v[j + 1]), nb.y);
+            const float x2 = fmaxf(__uint_as_float(v[j + 2]), nb.z), x3 = fmaxf(__uint_as_float(v[j + 3]), nb.w);
+            acc[(j >> 2) & 1] = ffma2(pack2(w.x, w.y), pack2(x0, x1), acc[(j >> 2) & 1]);
+            acc[2 + ((j >> 2) & 1)] = ffma2(pack2(w.z, w.w), pack2(x2, x3), acc[2 + ((j >> 2) & 1)]);
+          }
+        }
+        float a8[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) unpack2(acc[j], a8[2 * j], a8[2 * j + 1]);
+        part = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+      }
+    }
+    // next tile's A0 (sub 0) and the next layer-1 UMMA as soon as D is free
+    if (first && has_next) {
+      if (mode == MODE_PREDICT) {
+        make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
+      } else {
+        odometer_step(p.R, p.dD, D);
+        make_a0_sweep<PREC>(p, slut, D, a0);
+      }
+      put_a0();
+    }
+    if (tr) trace_ev(p, s, jr, 5);
+    if (C::NSUB > 1 && !last) red[(s * C::NSUB + q) * TILE_M + row] = part;
+    if (has_next) issue(0);  // includes the slot barrier: partials are visible after it
+    else named_bar_sync(bar_id, 128 * C::NSUB);
+    if (tr) trace_ev(p, s, jr, 6);
+    if (last) {
+      float t = 0.0f;
+#pragma unroll
+      for (int qq = 0; qq + 1 < C::NSUB; ++qq) t += red[(s * C::NSUB + qq) * TILE_M + row];
+      t = t + part + p.c_out;
+      if (mode == MODE_TOPK) {
+        const uint32_t key = f2key(t);
+        const bool pass = valid && key <= ts.misc[2];
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, pass);
+        if (m) {
+          const uint32_t n = __popc(m);
+          if (ncand + n > CAND_CAP) {
+            lock_acquire(ts, lane);
+            warp_merge(ts, mycand, ncand, p.k, lane);
+            lock_release(ts, lane);
+            ncand = 0;
+          }
+          if (pass) {
+            const uint32_t pos = ncand + __popc(m & ((1u << lane) - 1u));
+            mycand[pos].idx = I;
+            mycand[pos].key = key;
+            mycand[pos].pad = 0;
+          }
+          ncand += n;
+          __syncwarp();
+        }
+      } else if (valid) {
+        p.t_dense[I - p.begin] = t;
+      }
+    }
+    I = In;
+  }
+  if (last && mode == MODE_TOPK && ncand) {
+    lock_acquire(ts, lane);
+    warp_merge(ts, mycand, ncand, p.k, lane);
+    lock_release(ts, lane);
+  }
+
+  // ---- teardown
+  tc_fence_before();
+  __syncthreads();
+  if (mode == MODE_TOPK) {
+    const surr_record* L = ts.lists + (size_t)ts.misc[1] * p.k;
+    for (uint32_t i = threadIdx.x; i < p.k; i += blockDim.x) p.recs[(size_t)blockIdx.x * p.k + i] = L[i];
+  }
+  if (warp == 0) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+}  // namespace surr

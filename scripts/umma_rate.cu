@@ -64,6 +64,29 @@ __global__ void __launch_bounds__(256, 1) bench(int mode, uint32_t N, int iters,
       out[blockIdx.x * 2] = t1 - t0;
       out[blockIdx.x * 2 + 1] = (unsigned long long)iters * batch;
     }
+  } else if (mode == 7) {
+    // unrolled 8 tf32 UMMAs (K = 8 each) per commit, converged warp 0, elected lane
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((128u >> 4) << 24);
+    const uint64_t b0 = bdesc(sb, sbo);
+    if (warp == 0) {
+      uint32_t ph = 0;
+      t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        if (elect_one()) {
+#pragma unroll
+          for (int b = 0; b < 8; ++b) umma_tf32_ts(base, base + 256 + b * 8, b0 + (uint64_t)(b * 16), idesc, b > 0);
+          umma_commit(&bars[0]);
+        }
+        __syncwarp();
+        mbar_wait(&bars[0], ph);
+        ph ^= 1;
+      }
+      t1 = clock64();
+      if (lane == 0) {
+        out[blockIdx.x * 2] = t1 - t0;
+        out[blockIdx.x * 2 + 1] = (unsigned long long)iters * 8;
+      }
+    }
   } else if (mode == 5 || mode == 6) {
     // unrolled issue of 8 UMMAs per commit from a converged warp (elected lane);
     // issuer = warp 0 (mode 5) or warp 7 (mode 6); warps 1..6 burn ALU meanwhile
@@ -159,7 +182,8 @@ int main() {
   cudaMalloc(&d, 148 * 2 * 8);
   std::vector<unsigned long long> h(148 * 2);
   struct C { int mode; uint32_t N; int iters, batch; const char* what; };
-  C cs[] = {{5, 128, 200, 0, "unrolled x8, issuer warp0, idle others"}, {5, 64, 200, 0, "  same N=64"},
+  C cs[] = {{7, 128, 200, 0, "tf32 unrolled x8 N=128"}, {7, 64, 200, 0, "tf32 unrolled x8 N=64"}, {7, 256, 200, 0, "tf32 unrolled x8 N=256"},
+            {5, 128, 200, 0, "bf16 unrolled x8 N=128"},{5, 128, 200, 0, "unrolled x8, issuer warp0, idle others"}, {5, 64, 200, 0, "  same N=64"},
             {5, 128, 200, 1, "unrolled x8, issuer warp0, busy others"}, {6, 128, 200, 1, "unrolled x8, issuer warp7, busy others"},
             {6, 64, 200, 1, "  same N=64 warp7 busy"}, {6, 256, 200, 1, "  same N=256 warp7 busy"},{4, 128, 50, 64, "elected N=128 x64"}, {4, 64, 50, 64, "elected N=64 x64"},
             {4, 256, 50, 64, "elected N=256 x64"}, {4, 128, 200, 9, "elected N=128 x9 per commit"},{2, 128, 50, 64, "SS N=128 x64"}, {2, 64, 50, 64, "SS N=64 x64"}, {2, 256, 50, 64, "SS N=256 x64"},
@@ -167,7 +191,7 @@ int main() {
             {0, 128, 50, 64, "N=128 x64"},                {0, 64, 50, 64, "N=64 x64"},
             {0, 256, 50, 64, "N=256 x64"},                {0, 128, 400, 1, "N=128 x1 (issue+commit+wait)"},
             {1, 128, 400, 1, "ping-pong MMA->warp->MMA, N=128"}, {1, 64, 400, 1, "ping-pong N=64"}};
-  for (int rep = 0; rep < 2; ++rep)
+  for (int rep = 0; rep < 1; ++rep)
   for (auto& c : cs) {
     for (int grid : {148}) {
       bench<<<grid, 256, 80 * 1024>>>(c.mode, c.N, c.iters, c.batch, d);

@@ -15,9 +15,9 @@ def _bf16(x):
     return r.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
-def _tf32(x):  # round to nearest, ties away (cvt.rna.tf32.f32)
+def _tf32(x):  # round to nearest even (cvt.rn.tf32.f32)
     a = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
-    r = ((a + 0x1000) >> 13) << 13
+    r = ((a + 0xFFF + ((a >> 13) & 1)) >> 13) << 13
     return r.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
