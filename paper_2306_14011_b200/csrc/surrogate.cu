@@ -176,8 +176,10 @@ bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg 
     if (H == 64) { *ki = spg == 4 ? kinfo3<64, 4>() : kinfo3<64, 2>(); return true; }
     if (H == 128) { *ki = spg == 4 ? kinfo3<128, 4>() : kinfo3<128, 2>(); return true; }
   }
-  // TF32-family nets with at most one hidden->hidden layer: self-issuing, split columns
-  if (prec != PREC_BF16 && NL <= 2) {
+  // FP32 (3xTF32) nets with at most one hidden->hidden layer: self-issuing, split
+  // columns, separate D2 region (measured faster than the general kernel; for
+  // 1xTF32 the general two-slot kernel measured faster, 572 vs 482 TFLOP/s)
+  if (prec == PREC_FP32 && NL <= 2) {
 #define CASE5(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo5<P_, H_>(); return true; }
     CASE5(PREC_FP32, 32) CASE5(PREC_FP32, 64) CASE5(PREC_FP32, 128)

@@ -20,7 +20,11 @@ namespace surr {
 template <int PREC, int H>
 struct Cfg5 {
   static constexpr int A_COLS = PREC == PREC_FP32 ? 2 * H : H;
-  static constexpr int SLOT_COLS = H + A_COLS;
+  // FP32: the last layer accumulates into its own region Y = D2, so the next
+  // tile's layer-1 UMMA (into D1) overlaps this tile's final layer (reads D2)
+  static constexpr bool SEP_Y = PREC == PREC_FP32;
+  static constexpr int SLOT_COLS = H + A_COLS + (SEP_Y ? H : 0);
+  static constexpr int Y_COL = H + A_COLS;  // D2 region (SEP_Y)
   static constexpr int NSLOT = 512 / SLOT_COLS >= 2 ? 2 : 1;
   static constexpr int NSUB0 = NSLOT == 2 ? 2 : 4;
   static constexpr int NSUB = (H / 32 < NSUB0) ? H / 32 : NSUB0;  // warpgroups per slot
@@ -117,12 +121,13 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
             umma_tf32_ts(dslot, a + C::A0_LO + kk * 8, d_b1 + kk * 16, idesc, 1u);
           }
         } else {
+          const uint32_t d2 = dslot + (C::SEP_Y ? C::Y_COL : 0);
 #pragma unroll
           for (int kk = 0; kk < H / 8; ++kk) {
-            umma_tf32_ts(dslot, a + kk * 8, d_b2 + kk * 16, idesc, kk > 0);
+            umma_tf32_ts(d2, a + kk * 8, d_b2 + kk * 16, idesc, kk > 0);
             if (C::THREE_H) {
-              umma_tf32_ts(dslot, a + kk * 8, d_b2lo + kk * 16, idesc, 1u);
-              umma_tf32_ts(dslot, a + H + kk * 8, d_b2 + kk * 16, idesc, 1u);
+              umma_tf32_ts(d2, a + kk * 8, d_b2lo + kk * 16, idesc, 1u);
+              umma_tf32_ts(d2, a + H + kk * 8, d_b2 + kk * 16, idesc, 1u);
             }
           }
         }
@@ -185,13 +190,27 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
         tmem_wait_st();
         if (tr) trace_ev(p, s, jr, 2);
         issue(1);
+        if (C::SEP_Y && first && has_next) {  // next tile's digits / row while L2 runs
+          if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
+          else odometer_step(p.R, p.dD, D);
+        }
       } else {
         // a7: final-layer partial over this sub's columns (relu(x + b) = max(x, -b) + b)
+        if (C::SEP_Y && has_next) {
+          // D2 ready => L2 no longer reads A: store the next A0 there and start
+          // the next tile's layer 1 (into D1) before reading D2
+          if (first) {
+            if (mode != MODE_PREDICT) make_a0_sweep<PREC>(p, slut, D, a0);
+            put_a0();
+          }
+          issue(0);
+        }
+        const uint32_t fcol = dcol + (C::SEP_Y ? C::Y_COL : 0);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
         for (int c = 0; c < C::CPS / 32; ++c) {
           uint32_t v[32];
-          tmem_ld32(dcol + c * 32, v);
+          tmem_ld32(fcol + c * 32, v);
           tmem_wait_ld();
           // w and -b of this sub's columns: broadcast 16-byte shared-memory loads
           // (the column offset depends on the warpgroup, so no constant-bank operands)
@@ -213,7 +232,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
       }
     }
     // next tile's A0 (sub 0) and the next layer-1 UMMA as soon as D is free
-    if (first && has_next) {
+    if (!C::SEP_Y && first && has_next) {
       if (mode == MODE_PREDICT) {
         make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
       } else {
@@ -224,7 +243,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
     }
     if (tr) trace_ev(p, s, jr, 5);
     if (C::NSUB > 1 && !last) red[(s * C::NSUB + q) * TILE_M + row] = part;
-    if (has_next) issue(0);  // includes the slot barrier: partials are visible after it
+    if (!C::SEP_Y && has_next) issue(0);  // includes the slot barrier: partials are visible after it
     else named_bar_sync(bar_id, 128 * C::NSUB);
     if (tr) trace_ev(p, s, jr, 6);
     if (last) {

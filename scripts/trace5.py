@@ -20,3 +20,7 @@ for s in range(2):
     print("slot", s, "cycles per tile", np.median(np.diff(d[:, 0])))
     for a, b, lab in [(0, 1, "wait L1"), (1, 2, "epi1"), (2, 3, "L2 (issue..done)"), (3, 5, "final"), (5, 6, "A0+issue L1 / bar")]:
         print(f"   {lab:20s} {np.median(d[:, b] - d[:, a]):8.0f}")
+d = t[10:40, 0]
+print("raw events (cycles after loop top) for 3 tiles:")
+for j in range(3):
+    print([int(x - d[j, 0]) for x in d[j, :7]])
