@@ -189,7 +189,9 @@ def main():
     from paper_2306_14011_b200.dist import shard_range
 
     torch.cuda.set_device(local)
-    if world > 1:
+    # under torchrun the collective path (records -> all_gather -> merge) runs even at world size 1
+    collective = "RANK" in os.environ
+    if collective:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     vl = workloads.space(wl.space)
     model = workloads.load_model(wl.weights)
@@ -207,7 +209,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
-        if world == 1:
+        if not collective:
             h.sweep_into(desc, k, idx, tt)
             return h.last_launches()
         n = h.sweep_records_into(desc, k, recs)
@@ -218,7 +220,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if collective:
         dist.barrier()
     h.kernel_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -226,7 +228,7 @@ def main():
     with ClockSampler(local) as clk:
         for s in range(args.steps):
             flush.zero_()                      # L2 flushed between timed steps (untimed)
-            if world > 1:
+            if collective:
                 dist.barrier()
             torch.cuda.synchronize()
             ev[s][0].record(stream)
@@ -237,7 +239,7 @@ def main():
     total_ms = sum(step_ms)
     k1_ms, k1_n = h.kernel_timing_get()
     h.kernel_timing(False)
-    if world > 1:
+    if collective:
         tms = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tms, op=dist.ReduceOp.MAX)
         total_ms = float(tms.item())
@@ -252,7 +254,31 @@ def main():
 
     # end to end through the public API: value table H2D + result D2H every step
     e2e = None
-    if world == 1:
+    if collective:
+        # end to end at N ranks: table rebuilt + uploaded, shard sweep, all_gather,
+        # merge, k results copied to pinned host memory; wall time, max over ranks
+        hidx = torch.empty(k, dtype=torch.int64, pin_memory=True)
+        ht = torch.empty(k, dtype=torch.float32, pin_memory=True)
+
+        def e2e_step():
+            h.reset_cache()
+            step()
+            hidx.copy_(idx, non_blocking=True)
+            ht.copy_(tt, non_blocking=True)
+            torch.cuda.synchronize()
+
+        for _ in range(2):
+            e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": N * args.steps / float(e2e_s.item()), "unit": "evals/s",
+               "h2d_bytes_per_step": int(h.lut_bytes() + desc.radix.nbytes + desc.values.nbytes),
+               "d2h_bytes_per_step": int(k * (8 + 4))}
+    else:
         hidx, ht = np.empty(k, np.uint64), np.empty(k, np.float32)
         for _ in range(2):
             h.sweep_host(vl, k, desc=desc, out=(hidx, ht))
@@ -274,7 +300,8 @@ def main():
                           "net": "-".join(map(str, model["widths"])), "k": k, "precision": precision,
                           "weights": f"oracle-trained ({wl.weights})",
                           "l2": "flushed between timed steps (256 MiB write, untimed); inputs generated on chip",
-                          "parallelism": f"dp{world} (index-range shards, 1 all_gather + merge)"},
+                          "parallelism": f"dp{world} (index-range shards, 1 all_gather + merge)"
+                          + ("" if collective else " [single process: no collective]")},
                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": achieved / peak, "traffic": traffic,
                             "peak_source": f"{src} bf16 burst x {PEAK_RATIO[precision]} ({precision})",
@@ -288,7 +315,11 @@ def main():
         elif not args.no_cpu_baseline:
             out["cpu_baseline"] = None
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if collective:
+        # every rank holds the identical merged top-k; check it against rank 0's
+        ref = idx.clone()
+        dist.broadcast(ref, 0)
+        assert torch.equal(ref, idx), "ranks disagree on the merged top-k"
         dist.barrier()
         dist.destroy_process_group()
 

@@ -172,6 +172,10 @@ surr_status surrogate_kernel_timing_get(surrogate_t *h, double *total_ms, uint32
  * Layout: (round * 4 + slot) * 16 + event (see sweep_kernel3.cuh). */
 surr_status surrogate_debug_trace(surrogate_t *h, unsigned long long *trace_dev, uint32_t n);
 
+/* Drop the cached value table: the next sweep call rebuilds it from the
+ * descriptor and uploads it again (used to time end-to-end sweeps). */
+surr_status surrogate_reset_cache(surrogate_t *h);
+
 /* Bytes of the value lookup table of the cached space (the per-sweep H2D of
  * surrogate_sweep_host). */
 uint32_t surrogate_table_bytes(const surrogate_t *h);

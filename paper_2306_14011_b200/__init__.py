@@ -23,7 +23,7 @@ EXPORTS = [
     "surrogate_predict", "surrogate_sweep", "surrogate_sweep_host", "surrogate_eval_range",
     "surrogate_merge_topk", "surrogate_sweep_records", "surrogate_decode_range", "surrogate_space_size",
     "surrogate_kernel_timing", "surrogate_kernel_timing_get", "surrogate_last_launches",
-    "surrogate_selftest_umma", "surrogate_table_bytes", "surrogate_debug_trace",
+    "surrogate_selftest_umma", "surrogate_table_bytes", "surrogate_debug_trace", "surrogate_reset_cache",
 ]
 
 
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         L.surrogate_last_launches.restype = u32
         L.surrogate_selftest_umma.argtypes = [i32, i32, u32, u32, vp, vp, vp]
         L.surrogate_debug_trace.argtypes = [vp, vp, u32]
+        L.surrogate_reset_cache.argtypes = [vp]
         L.surrogate_table_bytes.argtypes = [vp]
         L.surrogate_table_bytes.restype = u32
         for name in EXPORTS:
@@ -234,6 +235,10 @@ class Surrogate:
         _check(lib().surrogate_merge_topk(self.h, ctypes.c_void_p(recs.data_ptr()), lists, k_in, k,
                                           ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(t.data_ptr()),
                                           None, _stream_ptr(stream)), self.h)
+
+    def reset_cache(self):
+        """Drop the cached value table (next sweep rebuilds + uploads it)."""
+        _check(lib().surrogate_reset_cache(self.h), self.h)
 
     def lut_bytes(self) -> int:
         """Bytes of the value table uploaded by the last sweep (the per-step H2D)."""

@@ -750,6 +750,12 @@ surr_status surrogate_debug_trace(surrogate_t* h, unsigned long long* trace_dev,
   return SURR_OK;
 }
 
+surr_status surrogate_reset_cache(surrogate_t* h) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  h->space_valid = false;
+  return SURR_OK;
+}
+
 surr_status surrogate_kernel_timing(surrogate_t* h, int enable) {
   if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
   h->timing = enable != 0;
