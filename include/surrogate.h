@@ -80,8 +80,10 @@ typedef struct {
  * x_scale == 0 is treated as 1.  The output is t = y_mean + y_scale * yhat
  * (SURVEY G4).  Constant device features are raw
  * values appended after the P tuning parameters; they are folded into the
- * first-layer bias at load time.  Current kernel envelope: E == 1,
- * H in {32, 64, 128}, 1 <= L-1 <= SURR_MAX_HIDDEN_LAYERS, P + 1 <= 32. */
+ * first-layer bias at load time.  Ensembles (E <= 64) run one fused pass per
+ * member: members 0..E-2 accumulate t in an fp32 device buffer (chunks of
+ * 2^28 configs), the last one averages and emits.  Kernel envelope:
+ * H in {32, 64, 128}, 1 <= L-1 <= SURR_MAX_HIDDEN_LAYERS, P + 1 <= 16. */
 typedef struct {
   uint32_t num_layers;           /* L affine layers */
   const uint32_t *widths;        /* [L + 1] */

@@ -35,7 +35,10 @@ struct surrogate {
   std::vector<uint8_t> wimg;
   void* d_w = nullptr;
   size_t d_w_cap = 0;
-  KParams mp{};  // model part of the kernel parameters
+  KParams mp{};  // model part of the kernel parameters (member 0)
+  std::vector<KParams> members;  // per-member model parameters (ensemble)
+  float* d_acc = nullptr;        // ensemble accumulation buffer (fp32 per config of a chunk)
+  size_t d_acc_cap = 0;
   double* d_zshift = nullptr;
   double* d_zscale = nullptr;
   std::vector<double> hshift, hscale;  // host copies of the input affine map
@@ -318,9 +321,9 @@ struct Launch {
   KParams p;
 };
 
-surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L) {
+surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L, uint32_t member = 0) {
   if (!get_kernel(h->prec, h->H, h->NL, &L->ki, h->spg)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
-  KParams p = h->mp;
+  KParams p = h->members.empty() ? h->mp : h->members[member];
   const KParams& s = h->sp;
   if (mode != MODE_PREDICT) {
     memcpy(p.R, s.R, sizeof p.R);
@@ -409,6 +412,66 @@ surr_status launch_merge(surrogate* h, const surr_record* in, uint32_t lists, ui
   return SURR_OK;
 }
 
+// K1 over [begin, end) in `mode`, with the ensemble passes when E > 1: per
+// chunk of <= 2^28 configs, members 0..E-2 accumulate t into d_acc and the last
+// member averages and emits (top-k records at recs + lists * k, or dense t,
+// or predict rows).  Returns the number of record lists written.
+surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, float* t_dense, const float* x,
+                   cudaStream_t st, uint32_t* lists_out) {
+  const uint32_t E = (uint32_t)std::max<size_t>(1, h->members.size());
+  const uint64_t chunk = E == 1 ? (end - begin) : (1ull << 28);
+  // record lists of every chunk's final pass
+  uint64_t lists = 0;
+  for (uint64_t c0 = begin; c0 < end; c0 += chunk) {
+    Launch L;
+    surr_status rc = plan(h, c0, std::min(end, c0 + chunk), k, mode, &L);
+    if (rc) return rc;
+    lists += (uint64_t)L.grid;
+  }
+  if (mode == MODE_TOPK) {
+    surr_status rc = ensure_recs(h, (size_t)lists * k);
+    if (rc) return rc;
+  }
+  if (E > 1) {
+    const size_t need = (size_t)std::min<uint64_t>(chunk, end - begin);
+    if (need > h->d_acc_cap) {
+      cudaFree(h->d_acc);
+      h->d_acc = nullptr;
+      if (cudaMalloc(&h->d_acc, need * sizeof(float)) != cudaSuccess) return fail(h, SURR_E_OOM, "cudaMalloc acc");
+      h->d_acc_cap = need;
+    }
+  }
+  uint64_t done = 0;
+  for (uint64_t c0 = begin; c0 < end; c0 += chunk) {
+    const uint64_t c1 = std::min(end, c0 + chunk);
+    int grid = 0;
+    for (uint32_t e = 0; e < E; ++e) {
+      const bool last = e + 1 == E;
+      const int m = mode == MODE_PREDICT ? MODE_PREDICT : (last ? mode : MODE_DENSE);
+      Launch L;
+      surr_status rc = plan(h, c0, c1, k, m, &L, e);
+      if (rc) return rc;
+      grid = L.grid;
+      if (E > 1) {
+        L.p.acc_mode = e == 0 ? 1u : (last ? 3u : 2u);
+        L.p.t_acc = h->d_acc;
+        L.p.acc_base = c0;
+        L.p.inv_e = 1.0f / (float)E;
+      }
+      L.p.recs = h->d_recs + done * k;
+      L.p.t_dense = t_dense ? t_dense + (c0 - begin) : nullptr;
+      L.p.x = x;
+      L.p.trace = h->trace;
+      L.p.trace_n = h->trace_n;
+      rc = launch(h, L, m, st);
+      if (rc) return rc;
+    }
+    done += (uint64_t)grid;
+  }
+  *lists_out = (uint32_t)done;
+  return SURR_OK;
+}
+
 surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint64_t* idx_dev, float* t_dev,
                          surr_record* recs_dev, uint32_t* count_host, cudaStream_t st, bool force) {
   if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
@@ -425,17 +488,10 @@ surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint
     // empty range: all-sentinel result through the merge kernel (zero lists)
     return launch_merge(h, h->d_recs, 0, k, k, idx_dev, t_dev, recs_dev, st);
   }
-  Launch L;
-  rc = plan(h, begin, end, k, MODE_TOPK, &L);
+  uint32_t lists = 0;
+  rc = run_k1(h, begin, end, k, MODE_TOPK, nullptr, nullptr, st, &lists);
   if (rc) return rc;
-  rc = ensure_recs(h, (size_t)L.grid * k);
-  if (rc) return rc;
-  L.p.recs = h->d_recs;
-  L.p.trace = h->trace;
-  L.p.trace_n = h->trace_n;
-  rc = launch(h, L, MODE_TOPK, st);
-  if (rc) return rc;
-  return launch_merge(h, h->d_recs, (uint32_t)L.grid, k, k, idx_dev, t_dev, recs_dev, st);
+  return launch_merge(h, h->d_recs, lists, k, k, idx_dev, t_dev, recs_dev, st);
 }
 
 }  // namespace
@@ -465,7 +521,7 @@ void surrogate_destroy(surrogate_t* h) {
   if (!h) return;
   cudaSetDevice(h->dev);
   cudaFree(h->d_w); cudaFree(h->d_lut); cudaFree(h->d_recs); cudaFree(h->d_merged);
-  cudaFree(h->d_zshift); cudaFree(h->d_zscale);
+  cudaFree(h->d_zshift); cudaFree(h->d_zscale); cudaFree(h->d_acc);
   for (auto e : h->ev) cudaEventDestroy(e);
   delete h;
 }
@@ -495,7 +551,8 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   const uint32_t L = m->num_layers;
   if (L < 2 || L - 1 > SURR_MAX_HIDDEN_LAYERS)
     return fail(h, SURR_E_UNSUPPORTED, "num_layers %u: need 1..%u hidden layers", L, SURR_MAX_HIDDEN_LAYERS);
-  if (m->ensemble != 1) return fail(h, SURR_E_UNSUPPORTED, "ensemble %u: only E == 1 in this build", m->ensemble);
+  if (m->ensemble < 1 || m->ensemble > 64) return fail(h, SURR_E_INVALID_ARG, "ensemble %u outside 1..64", m->ensemble);
+  const uint32_t E = m->ensemble;
   if (m->precision != SURR_PREC_BF16 && m->precision != SURR_PREC_FP32 && m->precision != SURR_PREC_TF32)
     return fail(h, SURR_E_INVALID_ARG, "precision %d", (int)m->precision);
   const uint32_t F = m->widths[0], H = m->widths[1];
@@ -507,7 +564,7 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     return fail(h, SURR_E_INVALID_ARG, "const features");
   const uint32_t P = F - m->num_const_features;
   if (P == 0 || P + 1 > (uint32_t)K0) return fail(h, SURR_E_UNSUPPORTED, "%u tuning parameters: need 1..15", P);
-  for (uint32_t l = 0; l < L; ++l)
+  for (uint32_t l = 0; l < E * L; ++l)
     if (!m->W[l] || !m->b[l]) return fail(h, SURR_E_INVALID_ARG, "null layer %u", l);
   CU(cudaSetDevice(h->dev));
 
@@ -518,98 +575,107 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     shift[j] = m->x_shift[j];
     scale[j] = m->x_scale[j] == 0.0 ? 1.0 : m->x_scale[j];
   }
-  // layer 1 operand rows: z_0..z_{P-1}, ones slot carrying b_1 + W1[const] z_const, zeros
-  const double* W1 = m->W[0];
-  std::vector<double> B1((size_t)K0 * H, 0.0);  // [k][n]
-  for (uint32_t kk = 0; kk < P; ++kk)
-    for (uint32_t n = 0; n < H; ++n) B1[(size_t)kk * H + n] = W1[(size_t)kk * H + n];
-  for (uint32_t n = 0; n < H; ++n) {
-    double b = m->b[0][n];
-    for (uint32_t c = 0; c < m->num_const_features; ++c) {
-      const double zc = (m->const_features[c] - shift[P + c]) / scale[P + c];
-      b += W1[(size_t)(P + c) * H + n] * zc;
-    }
-    B1[(size_t)P * H + n] = b;
-  }
-  const bool bf = prec == PREC_BF16;
-  const uint32_t esz = bf ? 2 : 4;
-  KernelInfo ki;
-  if (!get_kernel(prec, H, L - 1, &ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", H);
-  const bool bias_mma = ki.bias_mma;     // hidden biases as an extra UMMA K block
-  const uint32_t kstep = bf ? 16 : 8;
-  const uint32_t KH = H + (bias_mma ? kstep : 0);  // K extent of a hidden-layer B image
-  const bool lo1 = !bf;                  // layer 1 carries a lo part in both TF32 modes
-  const bool loh = prec == PREC_FP32;    // hidden layers carry a lo part (3xTF32)
-  const size_t b1_bytes = (size_t)H * K0 * esz;
-  const size_t bh_bytes = (size_t)H * KH * esz;
-  KParams& p = h->mp;
-  p = KParams{};
-  size_t off = 0;
-  p.off_b1 = (uint32_t)off; off += b1_bytes;
-  p.off_b1lo = lo1 ? (uint32_t)off : p.off_b1; off += lo1 ? b1_bytes : 0;
-  off = align_up(off, 128);
-  p.off_bh = (uint32_t)off;
-  p.lo_delta_h = (uint32_t)bh_bytes;
-  p.stride_bh = (uint32_t)align_up(bh_bytes * (loh ? 2 : 1), 128);
-  off += (size_t)(NL - 1) * p.stride_bh;
-  off = align_up(off, 16);
-  p.off_fin = (uint32_t)off;  // final-layer [w' (H floats), -b (H floats)] for shared-memory readers
-  off += 2ull * H * 4;
-  p.w_bytes = (uint32_t)align_up(std::max<size_t>(off, 128), 128);
-  std::vector<uint8_t> img(p.w_bytes, 0);
-
-  // pack src [K][N] (fan_in x fan_out, plus an optional bias row at k = K_src)
-  auto put = [&](size_t base, const double* src, uint32_t Ksrc, const double* bias, uint32_t K, uint32_t N,
-                 bool lo_part, size_t lo_base) {
-    for (uint32_t kk = 0; kk < K; ++kk)
-      for (uint32_t n = 0; n < N; ++n) {
-        double x = 0.0;
-        if (kk < Ksrc) x = src[(size_t)kk * N + n];
-        else if (kk == Ksrc && bias) x = bias[n];
-        const size_t o = pack_offset(n, kk, K, esz);
-        if (bf) {
-          uint16_t v = bf16_rne((float)x);
-          memcpy(&img[base + o], &v, 2);
-        } else {
-          uint32_t hi, lo;
-          tf32_split(x, &hi, &lo);
-          memcpy(&img[base + o], &hi, 4);
-          if (lo_part) memcpy(&img[lo_base + o], &lo, 4);
-        }
+  std::vector<KParams> mps(E);
+  std::vector<std::vector<uint8_t>> imgs(E);
+  for (uint32_t e = 0; e < E; ++e) {
+    // layer 1 operand rows: z_0..z_{P-1}, ones slot carrying b_1 + W1[const] z_const, zeros
+    const double* W1 = m->W[e * L + 0];
+    std::vector<double> B1((size_t)K0 * H, 0.0);  // [k][n]
+    for (uint32_t kk = 0; kk < P; ++kk)
+      for (uint32_t n = 0; n < H; ++n) B1[(size_t)kk * H + n] = W1[(size_t)kk * H + n];
+    for (uint32_t n = 0; n < H; ++n) {
+      double b = m->b[e * L + 0][n];
+      for (uint32_t c = 0; c < m->num_const_features; ++c) {
+        const double zc = (m->const_features[c] - shift[P + c]) / scale[P + c];
+        b += W1[(size_t)(P + c) * H + n] * zc;
       }
-  };
-  put(p.off_b1, B1.data(), K0, nullptr, K0, H, lo1, p.off_b1lo);
-  for (uint32_t l = 1; l < NL; ++l) {
-    const size_t base = p.off_bh + (size_t)(l - 1) * p.stride_bh;
-    put(base, m->W[l], H, bias_mma ? m->b[l] : nullptr, KH, H, loh, base + bh_bytes);
+      B1[(size_t)P * H + n] = b;
+    }
+    const bool bf = prec == PREC_BF16;
+    const uint32_t esz = bf ? 2 : 4;
+    KernelInfo ki;
+    if (!get_kernel(prec, H, L - 1, &ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", H);
+    const bool bias_mma = ki.bias_mma;     // hidden biases as an extra UMMA K block
+    const uint32_t kstep = bf ? 16 : 8;
+    const uint32_t KH = H + (bias_mma ? kstep : 0);  // K extent of a hidden-layer B image
+    const bool lo1 = !bf;                  // layer 1 carries a lo part in both TF32 modes
+    const bool loh = prec == PREC_FP32;    // hidden layers carry a lo part (3xTF32)
+    const size_t b1_bytes = (size_t)H * K0 * esz;
+    const size_t bh_bytes = (size_t)H * KH * esz;
+    KParams p{};
+    size_t off = 0;
+    p.off_b1 = (uint32_t)off; off += b1_bytes;
+    p.off_b1lo = lo1 ? (uint32_t)off : p.off_b1; off += lo1 ? b1_bytes : 0;
+    off = align_up(off, 128);
+    p.off_bh = (uint32_t)off;
+    p.lo_delta_h = (uint32_t)bh_bytes;
+    p.stride_bh = (uint32_t)align_up(bh_bytes * (loh ? 2 : 1), 128);
+    off += (size_t)(NL - 1) * p.stride_bh;
+    off = align_up(off, 16);
+    p.off_fin = (uint32_t)off;  // final-layer [w' (H floats), -b (H floats)] for shared-memory readers
+    off += 2ull * H * 4;
+    p.w_bytes = (uint32_t)align_up(std::max<size_t>(off, 128), 128);
+    std::vector<uint8_t> img(p.w_bytes, 0);
+
+    // pack src [K][N] (fan_in x fan_out, plus an optional bias row at k = K_src)
+    auto put = [&](size_t base, const double* src, uint32_t Ksrc, const double* bias, uint32_t K, uint32_t N,
+                   bool lo_part, size_t lo_base) {
+      for (uint32_t kk = 0; kk < K; ++kk)
+        for (uint32_t n = 0; n < N; ++n) {
+          double x = 0.0;
+          if (kk < Ksrc) x = src[(size_t)kk * N + n];
+          else if (kk == Ksrc && bias) x = bias[n];
+          const size_t o = pack_offset(n, kk, K, esz);
+          if (bf) {
+            uint16_t v = bf16_rne((float)x);
+            memcpy(&img[base + o], &v, 2);
+          } else {
+            uint32_t hi, lo;
+            tf32_split(x, &hi, &lo);
+            memcpy(&img[base + o], &hi, 4);
+            if (lo_part) memcpy(&img[lo_base + o], &lo, 4);
+          }
+        }
+    };
+    put(p.off_b1, B1.data(), K0, nullptr, K0, H, lo1, p.off_b1lo);
+    for (uint32_t l = 1; l < NL; ++l) {
+      const size_t base = p.off_bh + (size_t)(l - 1) * p.stride_bh;
+      put(base, m->W[e * L + l], H, bias_mma ? m->b[e * L + l] : nullptr, KH, H, loh, base + bh_bytes);
+    }
+    // final layer: t = y_mean + y_scale (sum_j w_j relu(D_j + b_j) + b_out)
+    //            = c' + sum_j w'_j max(D_j, -b_j),  w' = y_scale w,  c' = y_mean + y_scale (b_out + sum w b)
+    // (b_j = 0 here when the bias is already in D: layer 1, or folded into the UMMA)
+    const double* Wout = m->W[e * L + NL];
+    const double bout = m->b[e * L + NL][0];
+    const double* bl = (NL >= 2 && !bias_mma) ? m->b[e * L + NL - 1] : nullptr;
+    double cacc = bout;
+    for (uint32_t n = 0; n < H; ++n) {
+      const double bj = bl ? bl[n] : 0.0;
+      p.fin_nb[n] = (float)(-bj);
+      // kernels with the bias in the UMMA evaluate w relu(x) as (w/2) x + (w/2) |x|
+      p.fin_w[n] = (float)(m->y_scale * Wout[n] * (bias_mma ? 0.5 : 1.0));
+      cacc += Wout[n] * bj;
+    }
+    p.c_out = (float)(m->y_mean + m->y_scale * cacc);
+    {
+      float* fwb = reinterpret_cast<float*>(&img[p.off_fin]);
+      for (uint32_t n = 0; n < H; ++n) { fwb[n] = p.fin_w[n]; fwb[H + n] = p.fin_nb[n]; }
+    }
+    if (!bias_mma)
+      for (uint32_t l = 1; l + 1 < NL; ++l)
+        for (uint32_t n = 0; n < H; ++n) p.hbias[l - 1][n] = (float)m->b[e * L + l][n];
+    p.NL = NL;
+    p.sbo_b1 = (K0 / (16 / esz)) * 128;
+    p.sbo_bh = (KH / (16 / esz)) * 128;
+    p.idesc = make_idesc(bf ? 1 : 2, H, TILE_M);
+    p.P = P;
+    mps[e] = p;
+    imgs[e].swap(img);
   }
-  // final layer: t = y_mean + y_scale (sum_j w_j relu(D_j + b_j) + b_out)
-  //            = c' + sum_j w'_j max(D_j, -b_j),  w' = y_scale w,  c' = y_mean + y_scale (b_out + sum w b)
-  // (b_j = 0 here when the bias is already in D: layer 1, or folded into the UMMA)
-  const double* Wout = m->W[NL];
-  const double bout = m->b[NL][0];
-  const double* bl = (NL >= 2 && !bias_mma) ? m->b[NL - 1] : nullptr;
-  double cacc = bout;
-  for (uint32_t n = 0; n < H; ++n) {
-    const double bj = bl ? bl[n] : 0.0;
-    p.fin_nb[n] = (float)(-bj);
-    // kernels with the bias in the UMMA evaluate w relu(x) as (w/2) x + (w/2) |x|
-    p.fin_w[n] = (float)(m->y_scale * Wout[n] * (bias_mma ? 0.5 : 1.0));
-    cacc += Wout[n] * bj;
-  }
-  p.c_out = (float)(m->y_mean + m->y_scale * cacc);
-  {
-    float* fwb = reinterpret_cast<float*>(&img[p.off_fin]);
-    for (uint32_t n = 0; n < H; ++n) { fwb[n] = p.fin_w[n]; fwb[H + n] = p.fin_nb[n]; }
-  }
-  if (!bias_mma)
-    for (uint32_t l = 1; l + 1 < NL; ++l)
-      for (uint32_t n = 0; n < H; ++n) p.hbias[l - 1][n] = (float)m->b[l][n];
-  p.NL = NL;
-  p.sbo_b1 = (K0 / (16 / esz)) * 128;
-  p.sbo_bh = (KH / (16 / esz)) * 128;
-  p.idesc = make_idesc(bf ? 1 : 2, H, TILE_M);
-  p.P = P;
+  // all members' images back to back (each 128-byte aligned, same size)
+  const size_t wstride = imgs[0].size();
+  std::vector<uint8_t> img(wstride * E);
+  for (uint32_t e = 0; e < E; ++e) memcpy(img.data() + e * wstride, imgs[e].data(), wstride);
 
   if (img.size() > h->d_w_cap) {
     cudaFree(h->d_w);
@@ -618,7 +684,6 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     h->d_w_cap = img.size();
   }
   CU(cudaMemcpy(h->d_w, img.data(), img.size(), cudaMemcpyHostToDevice));
-  p.w_gmem = h->d_w;
   if (!h->d_zshift) {
     if (cudaMalloc(&h->d_zshift, 32 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&h->d_zscale, 32 * sizeof(double)) != cudaSuccess)
@@ -626,8 +691,13 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   }
   CU(cudaMemcpy(h->d_zshift, shift.data(), P * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(h->d_zscale, scale.data(), P * sizeof(double), cudaMemcpyHostToDevice));
-  p.zshift = h->d_zshift;
-  p.zscale = h->d_zscale;
+  for (uint32_t e = 0; e < E; ++e) {
+    mps[e].w_gmem = (const uint8_t*)h->d_w + e * wstride;
+    mps[e].zshift = h->d_zshift;
+    mps[e].zscale = h->d_zscale;
+  }
+  h->members.swap(mps);
+  h->mp = h->members[0];
   h->hshift = shift;
   h->hscale = scale;
   h->wimg.swap(img);
@@ -682,11 +752,8 @@ surr_status surrogate_eval_range(surrogate_t* h, const surr_space* space, float*
   if (rc) return rc;
   h->launches = 0;
   if (h->sp.end == h->sp.begin) return SURR_OK;
-  Launch L;
-  rc = plan(h, h->sp.begin, h->sp.end, 1, MODE_DENSE, &L);
-  if (rc) return rc;
-  L.p.t_dense = t_dev;
-  return launch(h, L, MODE_DENSE, (cudaStream_t)stream);
+  uint32_t lists = 0;
+  return run_k1(h, h->sp.begin, h->sp.end, 1, MODE_DENSE, t_dev, nullptr, (cudaStream_t)stream, &lists);
 }
 
 surr_status surrogate_predict(surrogate_t* h, const float* x_dev, uint64_t n, float* t_dev, void* stream) {
@@ -696,12 +763,8 @@ surr_status surrogate_predict(surrogate_t* h, const float* x_dev, uint64_t n, fl
   if (n == 0) return SURR_OK;
   if (!x_dev || !t_dev) return fail(h, SURR_E_INVALID_ARG, "null buffer");
   CU(cudaSetDevice(h->dev));
-  Launch L;
-  surr_status rc = plan(h, 0, n, 1, MODE_PREDICT, &L);
-  if (rc) return rc;
-  L.p.x = x_dev;
-  L.p.t_dense = t_dev;
-  return launch(h, L, MODE_PREDICT, (cudaStream_t)stream);
+  uint32_t lists = 0;
+  return run_k1(h, 0, n, 1, MODE_PREDICT, t_dev, x_dev, (cudaStream_t)stream, &lists);
 }
 
 surr_status surrogate_merge_topk(surrogate_t* h, const surr_record* recs_dev, uint32_t lists, uint32_t k_in,

@@ -76,6 +76,12 @@ struct KParams {
   float* t_dense;            // MODE_DENSE / MODE_PREDICT
   uint32_t smem_lut, smem_lists, smem_cand, smem_misc;  // byte offsets in dynamic smem
   uint32_t smem_a0, smem_ones;  // SS-form A0 tiles / ones block (4-slot kernel)
+  // ensemble passes: acc_mode 0 = single net; 1 = first member,
+  // t_acc[I - acc_base] = t; 2 = t_acc += t; 3 = last member, t = (t_acc + t) * inv_e
+  float* t_acc;
+  uint64_t acc_base;
+  uint32_t acc_mode;
+  float inv_e;
   // debug timeline (CTA 0 only): trace[ev] = clock64 of event ev, or null
   unsigned long long* trace;
   uint32_t trace_n;
@@ -83,6 +89,17 @@ struct KParams {
 
 static_assert(offsetof(KParams, fin_w) % 16 == 0 && offsetof(KParams, fin_nb) % 16 == 0,
               "epilogue constants must stay 16-byte aligned in the parameter bank (LDCU.128)");
+
+// Ensemble stage of one row's prediction; false = no output in this pass.
+// Uniform across a warp (depends on acc_mode only), so ballots stay legal.
+__device__ __forceinline__ bool ens_stage(const KParams& p, bool valid, uint64_t I, float& t) {
+  if (p.acc_mode == 0) return true;
+  float* a = p.t_acc + (I - p.acc_base);
+  if (p.acc_mode == 1) { if (valid) *a = t; return false; }
+  if (p.acc_mode == 2) { if (valid) *a += t; return false; }
+  t = ((valid ? *a : 0.0f) + t) * p.inv_e;  // members summed in order e = 0 .. E-1, mean in seconds
+  return true;
+}
 
 // debug timeline of CTA 0: slot s, tile round j, event e -> one clock64 stamp
 // (compiled in only with -DSURR_TRACE)
@@ -597,7 +614,8 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
       }
 
       // ---------------- outputs
-      if (mode == MODE_TOPK) {
+      if (!ens_stage(p, valid, I, t)) {
+      } else if (mode == MODE_TOPK) {
         const uint32_t key = f2key(t);
         // conservative filter on the key alone (a stale read only admits extra
         // candidates; the merge keeps the exact (key, idx) top-k)

@@ -363,8 +363,12 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       t = pa + pb;
     }
     t += p.c_out;
-    if (mode == MODE_TOPK) topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
-    else if (valid) p.t_dense[I - p.begin] = t;
+    if (!ens_stage(p, valid, I, t)) {
+    } else if (mode == MODE_TOPK) {
+      topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
+    } else if (valid) {
+      p.t_dense[I - p.begin] = t;
+    }
     if (tr) trace_ev(p, s, jr, 7);
     I = In;
   }

@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
 #pragma unroll
       for (int qq = 0; qq + 1 < C::NSUB; ++qq) t += red[(s * C::NSUB + qq) * TILE_M + row];
       t = t + part + p.c_out;
-      if (mode == MODE_TOPK) {
+      if (!ens_stage(p, valid, I, t)) {
+      } else if (mode == MODE_TOPK) {
         const uint32_t key = f2key(t);
         const bool pass = valid && key <= ts.misc[2];
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, pass);

@@ -180,3 +180,36 @@ def test_shard_invariance_bitwise(pk):
             recs.append(h.sweep_records(vl, k, b + lo, b + hi))
         mi, mt, _ = h.merge_topk(torch.cat(recs), W, k, k)
         assert torch.equal(mi, full_i) and torch.equal(mt, full_t)
+
+
+# ------------------------------------------------------------------ ensemble (cfg4)
+@pytest.mark.parametrize("device", ["C2075", "V100"])
+def test_cfg4_ensemble_combined_model(pk, device):
+    vl = workloads.space("cfg2")
+    model = workloads.with_device(workloads.load_model("cfg4_17-128-128-1_x8"),
+                                  workloads.device_features("onehot", device))
+    assert len(model["members"]) == 8 and model["widths"][0] == 17
+    h = _handle(pk, model, "bf16")
+    b, n = 77_777_777, (1 << 18) + 13
+    t = h.eval_range(vl, b, b + n).cpu().numpy()
+    ref = osweep.times(model, vl, b, b + n)
+    assert rel_err(t, ref, model["y_scale"]).max() <= TOL["bf16"]
+    idx, tk, cnt = h.sweep(vl, 16, b, b + n)
+    ri, rt = osweep.topk(model, vl, 16, b, b + n)
+    check_topk(idx.cpu().numpy().astype(np.uint64), tk.cpu().numpy(), ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL["bf16"], model["y_scale"])
+    # explicit batch through the same ensemble passes
+    X = ospace.values_of(ospace.decode(np.arange(b, b + 2000, dtype=np.uint64), workloads.radices("cfg2")), vl)
+    tp = h.predict(torch.tensor(X, dtype=torch.float32, device="cuda:0")).cpu().numpy()
+    assert np.array_equal(tp, t[:2000])
+
+
+def test_ensemble_fp32_path_and_chunking(pk):
+    # 3 random members on the FP32 path: 1e-5 against the oracle's mean
+    vl = workloads.space("cfg5")
+    model = workloads.random_net(vl, [64, 64], seed=21, ensemble=3)
+    h = _handle(pk, model, "fp32")
+    b, n = 5_000_000_000, 300_001
+    t = h.eval_range(vl, b, b + n).cpu().numpy()
+    ref = osweep.times(model, vl, b, b + n)
+    assert rel_err(t, ref, model["y_scale"]).max() <= TOL["fp32"]
