@@ -195,6 +195,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     vl = workloads.space(wl.space)
     model = workloads.load_model(wl.weights)
+    if wl.device_encoding:  # combined-training model: sweep for one target GPU (G3)
+        model = workloads.with_device(model, workloads.device_features(wl.device_encoding, wl.devices[-1]))
     N = int(np.prod([len(v) for v in vl]))
     lo, hi = shard_range(N, world, rank)
     h = pk.Surrogate(local).load(model, precision)
@@ -245,9 +247,11 @@ def main():
         total_ms = float(tms.item())
     value = N * args.steps / (total_ms / 1e3)
     # roofline of the dominant kernel (K1) from its own CUDA events on the launch stream
-    k1_avg_s = (k1_ms / max(k1_n, 1)) / 1e3
-    flops = algorithmic_flops(model["widths"]) * (hi - lo)
-    achieved = flops / k1_avg_s / 1e12
+    # (an E-member ensemble runs E K1 launches per step: all of them are counted)
+    members = len(model["members"])
+    k1_step_s = (k1_ms / args.steps) / 1e3
+    flops = algorithmic_flops(model["widths"]) * members * (hi - lo)
+    achieved = flops / k1_step_s / 1e12
     burst, sustained, src = load_peaks()
     peak = burst * PEAK_RATIO[precision]
     traffic = ncu_traffic(wl.name, precision)
@@ -297,7 +301,8 @@ def main():
                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": precision, "data": "synthetic",
                "config": {"workload": wl.name, "space": f"{wl.space}: {N} configs",
-                          "net": "-".join(map(str, model["widths"])), "k": k, "precision": precision,
+                          "net": "-".join(map(str, model["widths"])) + (f" x{members}" if members > 1 else ""),
+                          "k": k, "precision": precision,
                           "weights": f"oracle-trained ({wl.weights})",
                           "l2": "flushed between timed steps (256 MiB write, untimed); inputs generated on chip",
                           "parallelism": f"dp{world} (index-range shards, 1 all_gather + merge)"
@@ -305,8 +310,9 @@ def main():
                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": achieved / peak, "traffic": traffic,
                             "peak_source": f"{src} bf16 burst x {PEAK_RATIO[precision]} ({precision})",
-                            "kernel": "sweep_kernel (K1)", "k1_ms": k1_avg_s * 1e3,
-                            "flops_per_config": algorithmic_flops(model["widths"])},
+                            "kernel": "sweep_kernel (K1)", "k1_ms_per_step": k1_step_s * 1e3,
+                            "k1_launches_per_step": k1_n / args.steps,
+                            "flops_per_config": algorithmic_flops(model["widths"]) * members},
                "e2e": e2e, "gpu_launches": launches}
         with_clk = clk.summary()
         out["clocks"] = with_clk

@@ -369,7 +369,7 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
 surr_status launch(surrogate* h, Launch& L, int mode, cudaStream_t st) {
   CU(cudaFuncSetAttribute(L.ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->timing && mode == MODE_TOPK) {
+  if (h->timing) {  // every K1 launch (ensembles run one per member)
     if (h->ev_used + 2 > h->ev.size()) {
       for (int i = 0; i < 64; ++i) {
         cudaEvent_t e;
