@@ -21,6 +21,7 @@
 #include "sweep_kernel.cuh"
 #include "sweep_kernel3.cuh"
 #include "sweep_kernel5.cuh"
+#include "sweep_kernel_pair.cuh"
 
 using namespace surr;
 
@@ -143,7 +144,17 @@ struct KernelInfo {
   bool bias_mma;
   bool a0_smem = false;  // SS-form A0 tiles + ones block in shared memory
   uint32_t red_bytes = 0;  // shared-memory partials of split-column epilogues
+  bool pair = false;       // CTA-pair kernel (cluster of 2, cta_group::2, 256-row tiles)
 };
+
+template <int H, int SPG>
+KernelInfo kinfo_pair() {
+  using C = CfgPair<H>;
+  KernelInfo ki{(const void*)&sweep_kernel_pair<H, SPG>, 1, C::THREADS, true};
+  ki.red_bytes = C::NSUB * TILE_M * 4;
+  ki.pair = true;
+  return ki;
+}
 
 template <int PREC, int H>
 KernelInfo kinfo5() {
@@ -171,8 +182,16 @@ KernelInfo kinfo3() {
 bool uses_kernel3(int prec, uint32_t H, uint32_t NL) {
   return prec == PREC_BF16 && NL <= 2 && (H == 32 || H == 64 || H == 128);
 }
+bool uses_quads(int prec, uint32_t H, uint32_t NL) {  // kernels with 4-parameter decoder groups
+  return uses_kernel3(prec, H, NL) || (prec == PREC_BF16 && H == 256);
+}
 
 bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg = 2) {
+  // BF16 nets whose weights exceed one SM (H = 256): CTA pairs
+  if (prec == PREC_BF16 && H == 256) {
+    *ki = spg == 4 ? kinfo_pair<256, 4>() : kinfo_pair<256, 2>();
+    return true;
+  }
   // BF16 nets with at most one hidden->hidden layer: three tiles in flight
   if (uses_kernel3(prec, H, NL)) {
     if (H == 32) { *ki = spg == 4 ? kinfo3<32, 4>() : kinfo3<32, 2>(); return true; }
@@ -259,7 +278,7 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
     return e;
   };
   uint32_t spg = 2;
-  if (uses_kernel3(h->prec, h->H, h->NL) && table_entries(4) * 8 <= 64 * 1024) spg = 4;
+  if (uses_quads(h->prec, h->H, h->NL) && table_entries(4) * 8 <= 64 * 1024) spg = 4;
   const uint32_t ng = K0 / spg;
   const size_t esz = bf ? 2 * spg : 16;  // bf16: spg packed halves; tf32 (spg 2): hi pair + lo pair
   size_t entries = 0;
@@ -336,10 +355,15 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   }
   p.begin = begin;
   p.end = end;
-  p.num_tiles = (end - begin + TILE_M - 1) / TILE_M;
+  const uint64_t rows_per_tile = L->ki.pair ? 2 * TILE_M : TILE_M;
+  p.num_tiles = (end - begin + rows_per_tile - 1) / rows_per_tile;
   const int nslot = L->ki.nslot;
   uint64_t want = (p.num_tiles + nslot - 1) / nslot;
-  L->grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms, want));
+  if (L->ki.pair) {  // clusters of two CTAs, one 256-row tile per pair at a time
+    L->grid = 2 * (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms / 2, p.num_tiles));
+  } else {
+    L->grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms, want));
+  }
   p.dTiles = (uint32_t)(nslot * L->grid);
   if (mode != MODE_PREDICT) stride_digits(p.R, (uint64_t)p.dTiles * TILE_M, p.dD);
   p.k = mode == MODE_TOPK ? k : 1;
@@ -383,7 +407,23 @@ surr_status launch(surrogate* h, Launch& L, int mode, cudaStream_t st) {
     CU(cudaEventRecord(e0, st));
   }
   void* args[] = {(void*)&L.p, (void*)&mode};
-  CU(cudaLaunchKernel(L.ki.fn, dim3(L.grid), dim3(L.ki.threads), args, L.smem, st));
+  if (L.ki.pair) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(L.grid);
+    cfg.blockDim = dim3(L.ki.threads);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelExC(&cfg, L.ki.fn, args));
+  } else {
+    CU(cudaLaunchKernel(L.ki.fn, dim3(L.grid), dim3(L.ki.threads), args, L.smem, st));
+  }
   if (e1) CU(cudaEventRecord(e1, st));
   ++h->launches;
   return SURR_OK;
@@ -559,7 +599,8 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   if (m->widths[L] != 1) return fail(h, SURR_E_INVALID_ARG, "output width must be 1");
   for (uint32_t l = 1; l < L; ++l)
     if (m->widths[l] != H) return fail(h, SURR_E_UNSUPPORTED, "hidden widths must be equal");
-  if (H != 32 && H != 64 && H != 128) return fail(h, SURR_E_UNSUPPORTED, "hidden width %u not in {32,64,128}", H);
+  if (H != 32 && H != 64 && H != 128 && !(H == 256 && m->precision == SURR_PREC_BF16))
+    return fail(h, SURR_E_UNSUPPORTED, "hidden width %u not in {32,64,128} (256: BF16 only)", H);
   if (m->num_const_features > F || (m->num_const_features && !m->const_features))
     return fail(h, SURR_E_INVALID_ARG, "const features");
   const uint32_t P = F - m->num_const_features;
@@ -600,8 +641,11 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     const uint32_t KH = H + (bias_mma ? kstep : 0);  // K extent of a hidden-layer B image
     const bool lo1 = !bf;                  // layer 1 carries a lo part in both TF32 modes
     const bool loh = prec == PREC_FP32;    // hidden layers carry a lo part (3xTF32)
-    const size_t b1_bytes = (size_t)H * K0 * esz;
-    const size_t bh_bytes = (size_t)H * KH * esz;
+    // CTA-pair kernel: rank r's image holds B columns [r NR, (r+1) NR) of every layer
+    const uint32_t ranks = ki.pair ? 2 : 1;
+    const uint32_t NR = H / ranks;
+    const size_t b1_bytes = (size_t)NR * K0 * esz;
+    const size_t bh_bytes = (size_t)NR * KH * esz;
     KParams p{};
     size_t off = 0;
     p.off_b1 = (uint32_t)off; off += b1_bytes;
@@ -615,17 +659,19 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     p.off_fin = (uint32_t)off;  // final-layer [w' (H floats), -b (H floats)] for shared-memory readers
     off += 2ull * H * 4;
     p.w_bytes = (uint32_t)align_up(std::max<size_t>(off, 128), 128);
-    std::vector<uint8_t> img(p.w_bytes, 0);
+    p.w_rank_stride = p.w_bytes;
+    std::vector<uint8_t> img((size_t)p.w_bytes * ranks, 0);
 
-    // pack src [K][N] (fan_in x fan_out, plus an optional bias row at k = K_src)
+    // pack columns [n0, n0 + NR) of src [K][N] (fan_in x fan_out, plus an optional
+    // bias row at k = K_src) into a K-major core-matrix image at base
     auto put = [&](size_t base, const double* src, uint32_t Ksrc, const double* bias, uint32_t K, uint32_t N,
-                   bool lo_part, size_t lo_base) {
+                   uint32_t n0, bool lo_part, size_t lo_base) {
       for (uint32_t kk = 0; kk < K; ++kk)
-        for (uint32_t n = 0; n < N; ++n) {
+        for (uint32_t n = n0; n < n0 + NR; ++n) {
           double x = 0.0;
           if (kk < Ksrc) x = src[(size_t)kk * N + n];
           else if (kk == Ksrc && bias) x = bias[n];
-          const size_t o = pack_offset(n, kk, K, esz);
+          const size_t o = pack_offset(n - n0, kk, K, esz);
           if (bf) {
             uint16_t v = bf16_rne((float)x);
             memcpy(&img[base + o], &v, 2);
@@ -637,10 +683,13 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
           }
         }
     };
-    put(p.off_b1, B1.data(), K0, nullptr, K0, H, lo1, p.off_b1lo);
-    for (uint32_t l = 1; l < NL; ++l) {
-      const size_t base = p.off_bh + (size_t)(l - 1) * p.stride_bh;
-      put(base, m->W[e * L + l], H, bias_mma ? m->b[e * L + l] : nullptr, KH, H, loh, base + bh_bytes);
+    for (uint32_t r = 0; r < ranks; ++r) {
+      const size_t rb = (size_t)r * p.w_bytes;
+      put(rb + p.off_b1, B1.data(), K0, nullptr, K0, H, r * NR, lo1, rb + p.off_b1lo);
+      for (uint32_t l = 1; l < NL; ++l) {
+        const size_t base = rb + p.off_bh + (size_t)(l - 1) * p.stride_bh;
+        put(base, m->W[e * L + l], H, bias_mma ? m->b[e * L + l] : nullptr, KH, H, r * NR, loh, base + bh_bytes);
+      }
     }
     // final layer: t = y_mean + y_scale (sum_j w_j relu(D_j + b_j) + b_out)
     //            = c' + sum_j w'_j max(D_j, -b_j),  w' = y_scale w,  c' = y_mean + y_scale (b_out + sum w b)
@@ -649,17 +698,19 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     const double bout = m->b[e * L + NL][0];
     const double* bl = (NL >= 2 && !bias_mma) ? m->b[e * L + NL - 1] : nullptr;
     double cacc = bout;
+    std::vector<float> fw(H), fnb(H);
     for (uint32_t n = 0; n < H; ++n) {
       const double bj = bl ? bl[n] : 0.0;
-      p.fin_nb[n] = (float)(-bj);
+      fnb[n] = (float)(-bj);
       // kernels with the bias in the UMMA evaluate w relu(x) as (w/2) x + (w/2) |x|
-      p.fin_w[n] = (float)(m->y_scale * Wout[n] * (bias_mma ? 0.5 : 1.0));
+      fw[n] = (float)(m->y_scale * Wout[n] * (bias_mma ? 0.5 : 1.0));
       cacc += Wout[n] * bj;
+      if (n < 128) { p.fin_nb[n] = fnb[n]; p.fin_w[n] = fw[n]; }  // parameter-bank copy (H <= 128 kernels)
     }
     p.c_out = (float)(m->y_mean + m->y_scale * cacc);
-    {
-      float* fwb = reinterpret_cast<float*>(&img[p.off_fin]);
-      for (uint32_t n = 0; n < H; ++n) { fwb[n] = p.fin_w[n]; fwb[H + n] = p.fin_nb[n]; }
+    for (uint32_t r = 0; r < ranks; ++r) {
+      float* fwb = reinterpret_cast<float*>(&img[(size_t)r * p.w_bytes + p.off_fin]);
+      for (uint32_t n = 0; n < H; ++n) { fwb[n] = fw[n]; fwb[H + n] = fnb[n]; }
     }
     if (!bias_mma)
       for (uint32_t l = 1; l + 1 < NL; ++l)
@@ -667,7 +718,7 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     p.NL = NL;
     p.sbo_b1 = (K0 / (16 / esz)) * 128;
     p.sbo_bh = (KH / (16 / esz)) * 128;
-    p.idesc = make_idesc(bf ? 1 : 2, H, TILE_M);
+    p.idesc = make_idesc(bf ? 1 : 2, H, TILE_M * ranks);
     p.P = P;
     mps[e] = p;
     imgs[e].swap(img);

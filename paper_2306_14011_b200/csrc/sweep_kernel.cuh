@@ -63,6 +63,7 @@ struct KParams {
   uint32_t w_bytes;
   uint32_t off_b1, off_b1lo, off_bh, stride_bh, lo_delta_h;
   uint32_t off_fin;          // final-layer [w' (H), -b (H)] floats in the shared-memory image
+  uint32_t w_rank_stride;    // CTA-pair kernel: bytes between the two ranks' images
   uint32_t sbo_b1, sbo_bh;
   uint32_t idesc;
   float c_out;

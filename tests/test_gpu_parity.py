@@ -213,3 +213,46 @@ def test_ensemble_fp32_path_and_chunking(pk):
     t = h.eval_range(vl, b, b + n).cpu().numpy()
     ref = osweep.times(model, vl, b, b + n)
     assert rel_err(t, ref, model["y_scale"]).max() <= TOL["fp32"]
+
+
+# ------------------------------------------------------------------ CTA pairs (cfg3, H = 256)
+@pytest.mark.parametrize("hidden", [[256], [256, 256], [256, 256, 256]])
+def test_pair_kernel_random_nets(pk, hidden):
+    # cta_group::2 kernel over ragged ranges (odd pair-tile counts, tails inside rank 1)
+    vl = workloads.space("cfg3")
+    model = workloads.random_net(vl, hidden, seed=len(hidden) + 40)
+    h = _handle(pk, model, "bf16")
+    for b, n in [(0, 256 * 148 * 2 + 129), (1_279_000_000 - 70_001, 70_001), (5, 3)]:
+        t = h.eval_range(vl, b, b + n).cpu().numpy()
+        ref = osweep.times(model, vl, b, b + n)
+        e = rel_err(t, ref, model["y_scale"])
+        assert e.max() <= TOL["bf16"], f"{hidden} [{b},{b + n}): max rel err {e.max():.3e}"
+
+
+def test_cfg3_trained_slice_and_topk(pk):
+    vl = workloads.space("cfg3")
+    model = workloads.load_model("cfg3_14-256-256-256-1")
+    h = _handle(pk, model, "bf16")
+    b, n = 640_000_017, (1 << 18) + 333
+    t = h.eval_range(vl, b, b + n).cpu().numpy()
+    ref = osweep.times(model, vl, b, b + n)
+    assert rel_err(t, ref, model["y_scale"]).max() <= TOL["bf16"]
+    idx, tk, cnt = h.sweep(vl, 64, b, b + n)
+    ri, rt = osweep.topk(model, vl, 64, b, b + n)
+    assert cnt == 64
+    check_topk(idx.cpu().numpy().astype(np.uint64), tk.cpu().numpy(), ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL["bf16"], model["y_scale"])
+    X = ospace.values_of(ospace.decode(np.arange(b, b + 3000, dtype=np.uint64), workloads.radices("cfg3")), vl)
+    tp = h.predict(torch.tensor(X, dtype=torch.float32, device="cuda:0")).cpu().numpy()
+    assert np.array_equal(tp, t[:3000])
+
+
+def test_cfg3_full_sweep_reevaluated(pk):
+    vl = workloads.space("cfg3")
+    model = workloads.load_model("cfg3_14-256-256-256-1")
+    h = _handle(pk, model, "bf16")
+    idx, t, cnt = h.sweep(vl, 64)
+    idx = idx.cpu().numpy().astype(np.uint64)
+    t = t.cpu().numpy()
+    assert cnt == 64 and np.all(np.diff(t) >= 0)
+    assert rel_err(t, osweep.times_at(model, vl, idx), model["y_scale"]).max() <= TOL["bf16"]
