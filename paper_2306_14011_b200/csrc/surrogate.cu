@@ -151,7 +151,8 @@ template <int H, int SPG>
 KernelInfo kinfo_pair() {
   using C = CfgPair<H>;
   KernelInfo ki{(const void*)&sweep_kernel_pair<H, SPG>, 1, C::THREADS, true};
-  ki.red_bytes = C::NSUB * TILE_M * 4;
+  ki.a0_smem = true;
+  ki.red_bytes = TILE_M * 4;  // after the ones tile
   ki.pair = true;
   return ki;
 }
@@ -381,9 +382,9 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   off += 256;
   off = align_up(off, 1024);
   p.smem_a0 = (uint32_t)off;
-  off += std::max<size_t>(L->ki.a0_smem ? (size_t)nslot * 4096 : 0, L->ki.red_bytes);
+  off += L->ki.a0_smem ? (size_t)nslot * 4096 : L->ki.red_bytes;
   p.smem_ones = (uint32_t)off;
-  off += L->ki.a0_smem ? 4096 : 0;
+  off += L->ki.a0_smem ? 4096 + L->ki.red_bytes : 0;
   L->smem = off;
   if (L->smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "shared memory %zu B exceeds 227 KB", L->smem);
   L->p = p;
@@ -662,16 +663,25 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     p.w_rank_stride = p.w_bytes;
     std::vector<uint8_t> img((size_t)p.w_bytes * ranks, 0);
 
-    // pack columns [n0, n0 + NR) of src [K][N] (fan_in x fan_out, plus an optional
-    // bias row at k = K_src) into a K-major core-matrix image at base
+    // image row n of rank r <- output column gcol(r, n).  Single CTA: n.  CTA
+    // pair (N-half UMMAs of N = H/2, each CTA supplying H/4 B rows): rank r's
+    // rows [h H/4, (h+1) H/4) are columns h H/2 + r H/4 + [0, H/4) of half h
+    auto gcol = [&](uint32_t r, uint32_t n) -> uint32_t {
+      if (ranks == 1) return n;
+      const uint32_t Q = H / 4;
+      return (n / Q) * (H / 2) + r * Q + n % Q;
+    };
+    // pack src [K][N] (fan_in x fan_out, plus an optional bias row at k = K_src)
+    // rows of rank r into a K-major core-matrix image at base
     auto put = [&](size_t base, const double* src, uint32_t Ksrc, const double* bias, uint32_t K, uint32_t N,
-                   uint32_t n0, bool lo_part, size_t lo_base) {
+                   uint32_t r, bool lo_part, size_t lo_base) {
       for (uint32_t kk = 0; kk < K; ++kk)
-        for (uint32_t n = n0; n < n0 + NR; ++n) {
+        for (uint32_t nl = 0; nl < NR; ++nl) {
+          const uint32_t n = gcol(r, nl);
           double x = 0.0;
           if (kk < Ksrc) x = src[(size_t)kk * N + n];
           else if (kk == Ksrc && bias) x = bias[n];
-          const size_t o = pack_offset(n - n0, kk, K, esz);
+          const size_t o = pack_offset(nl, kk, K, esz);
           if (bf) {
             uint16_t v = bf16_rne((float)x);
             memcpy(&img[base + o], &v, 2);
@@ -685,10 +695,10 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     };
     for (uint32_t r = 0; r < ranks; ++r) {
       const size_t rb = (size_t)r * p.w_bytes;
-      put(rb + p.off_b1, B1.data(), K0, nullptr, K0, H, r * NR, lo1, rb + p.off_b1lo);
+      put(rb + p.off_b1, B1.data(), K0, nullptr, K0, H, r, lo1, rb + p.off_b1lo);
       for (uint32_t l = 1; l < NL; ++l) {
         const size_t base = rb + p.off_bh + (size_t)(l - 1) * p.stride_bh;
-        put(base, m->W[e * L + l], H, bias_mma ? m->b[e * L + l] : nullptr, KH, H, r * NR, loh, base + bh_bytes);
+        put(base, m->W[e * L + l], H, bias_mma ? m->b[e * L + l] : nullptr, KH, H, r, loh, base + bh_bytes);
       }
     }
     // final layer: t = y_mean + y_scale (sum_j w_j relu(D_j + b_j) + b_out)
@@ -718,7 +728,7 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     p.NL = NL;
     p.sbo_b1 = (K0 / (16 / esz)) * 128;
     p.sbo_bh = (KH / (16 / esz)) * 128;
-    p.idesc = make_idesc(bf ? 1 : 2, H, TILE_M * ranks);
+    p.idesc = ki.pair ? make_idesc(1, H / 2, 2 * TILE_M) : make_idesc(bf ? 1 : 2, H, TILE_M);
     p.P = P;
     mps[e] = p;
     imgs[e].swap(img);

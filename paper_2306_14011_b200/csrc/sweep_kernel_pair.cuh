@@ -2,34 +2,46 @@
 // fit one SM (BASELINE cfg 3: 14-256-256-256-1, 264 KB of BF16 weights).
 //
 // A cluster of two CTAs sweeps 256-row tiles: CTA rank r owns rows
-// [128 r, 128 r + 128) of every tile in its own TMEM (D: H fp32 columns, A:
-// H/2 packed bf16 columns, A0 and a ones block) and holds, in shared memory,
-// columns [r H/2, (r+1) H/2) of every layer's B operand (+ its bias K block) —
-// 140 KB per SM for cfg 3.  The leader CTA (rank 0) issues every
-// tcgen05.mma.cta_group::2 (M = 256, N = H, A from TMEM) after the eight (x NSUB)
-// warps of both CTAs have arrived on its "A ready" mbarrier (the peer's warps
-// arrive remotely, release at cluster scope), and commits each layer to the
-// "D ready" mbarrier of both CTAs (multicast).  Epilogues and the final FP32
-// layer are CTA-local: a row's H columns live in its own CTA's TMEM.  Columns
-// of an epilogue are split over NSUB warpgroups; the next tile's layer 1 is
-// released as soon as the final layer's TMEM loads are done.
+// [128 r, 128 r + 128) of every tile (its TMEM lanes) and holds, in shared
+// memory, 64 of the 128 output columns of each N-half of every layer's B
+// operand (+ its bias K block): 140 KB per SM for cfg 3.  The leader CTA's
+// issuer warp runs every tcgen05.mma.cta_group::2 (M = 256, N = H/2 per half).
+//
+// TMEM (512 columns) is two H-column regions used alternately by consecutive
+// layers.  A hidden epilogue writes its packed bf16 A IN PLACE over the region
+// it reads (chunk c is read before columns 16c.. are written), so layer l+1
+// reads A from one region while writing D into the other.  Every layer is
+// issued as two N-halves (own commit each) and streamed in K quarters:
+//   sub q (warps 4q .. 4q+3 of each CTA) owns output columns [q H/2, (q+1) H/2);
+//   it signals "A quarter 2q+j ready" after packing its j-th quarter, and the
+//   issuer runs those K-steps of the next layer for both N-halves right away,
+// so the epilogue of half a overlaps the MMA of half b and the epilogues
+// overlap the next layer's first K-steps.  The layer-1 operand A0 and the
+// bias "ones" block are SMEM tiles (SS form); a producer warp per CTA decodes
+// the next tile's A0 while the hidden layers run.
+//
+// warps 0-7: epilogue (2 subs x 4), warp 8: A0 producer, warp 9: MMA issuer
+// (leader CTA only).  Barriers (leader unless noted): A0F (2 producers), AQ[4]
+// (8 warps each), RF (16 warps: previous tile's final layer read its region),
+// DA / DB (both CTAs, multicast commits of the N-halves), A0E (both CTAs:
+// layer 1 done, A0 tile free).
 #pragma once
-#include "sweep_kernel.cuh"
+#include "sweep_kernel3.cuh"  // st_a0_smem, topk_offer
 
 namespace surr {
 
 template <int H>
 struct CfgPair {
-  static constexpr int NSUB = H >= 256 ? 2 : 1;         // warpgroups per CTA (split columns)
-  static constexpr int CPS = H / NSUB;                  // columns per sub
-  static constexpr int A_COL = H;                       // A operand: H/2 packed columns
-  static constexpr int A0_COL = H + H / 2;              // layer-1 operand (8 columns)
-  static constexpr int ONES_COL = A0_COL + 8;           // bias K block operand
-  static constexpr int NEED = ONES_COL + 8;
-  static constexpr int TMEM_COLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
-  static constexpr int THREADS = 128 * NSUB;
-  static_assert(NEED <= 512, "TMEM budget");
+  static constexpr int NSUB = 2;
+  static constexpr int HALF = H / 2;       // N per half-MMA = columns per sub
+  static constexpr int QC = H / 4;         // columns per K quarter
+  static constexpr int QSTEPS = QC / 16;   // UMMA K-steps per quarter
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int THREADS = 320;
+  static_assert(2 * H <= 512 && H % 64 == 0, "two H-column regions");
 };
+
+enum { PB_LOAD = 0, PB_A0F = 1, PB_AQ = 2, PB_RF = 6, PB_DA = 7, PB_DB = 8, PB_A0E = 9 };
 
 template <int H, int SPG>
 __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
@@ -42,9 +54,10 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_misc);  // [0] load, [1] A ready (leader), [2] D ready
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.smem_misc + 64);
-  float* red = reinterpret_cast<float*>(smem + p.smem_a0);           // [sub][row] partials
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_misc);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.smem_misc + 96);
+  uint8_t* a0tile = smem + p.smem_a0;
+  float* red = reinterpret_cast<float*>(smem + p.smem_ones + 4096);  // [row] partial of sub 0
   TopkShared ts;
   ts.lists = reinterpret_cast<surr_record*>(smem + p.smem_lists);
   ts.cand = reinterpret_cast<surr_record*>(smem + p.smem_cand);
@@ -53,17 +66,21 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
   // ---- setup (both CTAs)
   if (warp == 0) {
     if (lane == 0) {
-      mbar_init(&bars[0], 1);
-      mbar_init(&bars[1], 4 * C::NSUB * 2);  // every warp of both CTAs
-      mbar_init(&bars[2], 1);                // multicast commit from the leader
+      mbar_init(&bars[PB_LOAD], 1);
+      mbar_init(&bars[PB_A0F], 2);
+      for (int j = 0; j < 4; ++j) mbar_init(&bars[PB_AQ + j], 8);
+      mbar_init(&bars[PB_RF], 16);
+      mbar_init(&bars[PB_DA], 1);
+      mbar_init(&bars[PB_DB], 1);
+      mbar_init(&bars[PB_A0E], 1);
       fence_mbar_init();
       fence_proxy_async_smem();
       const uint8_t* wsrc = (const uint8_t*)p.w_gmem + (size_t)rank * p.w_rank_stride;
       const uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
-      mbar_arrive_expect_tx(&bars[0], total);
+      mbar_arrive_expect_tx(&bars[PB_LOAD], total);
       for (uint32_t off = 0; off < p.w_bytes; off += 32768u)
-        bulk_g2s(smem + off, wsrc + off, min(32768u, p.w_bytes - off), &bars[0]);
-      if (mode != MODE_PREDICT && p.lut_bytes) bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[0]);
+        bulk_g2s(smem + off, wsrc + off, min(32768u, p.w_bytes - off), &bars[PB_LOAD]);
+      if (mode != MODE_PREDICT && p.lut_bytes) bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[PB_LOAD]);
     }
     __syncwarp();
     tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
@@ -77,212 +94,252 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
       ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu;
     }
   }
+  if (warp >= 4 && warp < 8) {  // constant ones tile of the bias K step (bf16 1.0 in K slot 0)
+    uint32_t ones[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ones[j] = 0u;
+    ones[0] = 0x00003F80u;
+    st_a0_smem(smem + p.smem_ones, (warp - 4) * 32u + lane, ones);
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  const uint32_t q = warp >> 2;          // sub (column split)
-  const bool first = q == 0, last = q == C::NSUB - 1;
-  const uint32_t wq = warp & 3u;
-  const uint32_t row = wq * 32u + lane;
-  const uint32_t tl = (wq * 32u) << 16;
-  const uint32_t dcol = tmem_base + tl + q * C::CPS;
-  const uint32_t acol = tmem_base + tl + C::A_COL;
-  const uint32_t a0col = tmem_base + tl + C::A0_COL;
-  if (first) {  // constant ones block of the bias K step (each CTA's 128 lanes)
-    uint32_t ones[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) ones[j] = 0u;
-    ones[0] = 0x00003F80u;
-    tmem_st8(tmem_base + tl + C::ONES_COL, ones);
-    tmem_wait_st();
-  }
-  const uint8_t* slut = smem + p.smem_lut;
-  surr_record* mycand = ts.cand + (size_t)wq * CAND_CAP;
-  uint32_t ncand = 0;
-  const bool issuer = leader && warp == 0;
-  const uint32_t sb = smem_u32(smem);
-  const uint32_t idesc = p.idesc;  // M = 256, N = H
-  const uint64_t d_b1 = make_bdesc(sb + p.off_b1, p.sbo_b1);
   const uint32_t npairs = gridDim.x / 2;
   const uint64_t pair = blockIdx.x / 2;
-  uint32_t pha = 0, phd = 0;
-
-  // every warp of both CTAs -> leader's "A ready"; the leader's issuer waits and
-  // issues layer l's UMMA chain for the 256-row tile
-  auto arrive_and_issue = [&](uint32_t l) {
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive_cluster(&bars[1], 0);
-    if (issuer) {
-      mbar_wait_cluster(&bars[1], pha);
-      tc_fence_after();
-      if (elect_one()) {
-        if (l == 0) {
-          umma_f16_ts_pair(tmem_base, tmem_base + C::A0_COL, d_b1, idesc, 0u);
-        } else {
-          const uint64_t db = make_bdesc(sb + p.off_bh + (l - 1) * p.stride_bh, p.sbo_bh);
-#pragma unroll
-          for (int kk = 0; kk < H / 16; ++kk)
-            umma_f16_ts_pair(tmem_base, tmem_base + C::A_COL + kk * 8, db + kk * 16, idesc, kk > 0);
-          umma_f16_ts_pair(tmem_base, tmem_base + C::ONES_COL, db + (H / 16) * 16, idesc, 1u);
-        }
-        umma_commit_pair(&bars[2]);
-      }
-      __syncwarp();
-    }
-    pha ^= 1u;
-  };
-
-  uint64_t tile = pair;
-  uint64_t I = p.begin + tile * (2 * TILE_M) + rank * TILE_M + row;
   const uint64_t dI = (uint64_t)npairs * 2 * TILE_M;
-  uint32_t D[MAXG];
-  if (first && mode != MODE_PREDICT) init_digits_n<NG>(p.R, I, D);
-  mbar_wait(&bars[0], 0);
+  const uint8_t* slut = smem + p.smem_lut;
+  mbar_wait(&bars[PB_LOAD], 0);
 
-  A0Regs a0;
-  if (tile < p.num_tiles) {
-    if (first) {
-      if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, I < p.end ? I : p.begin, a0);
-      else if (SPG == 4) make_a0_sweep4(p, slut, D, a0);
-      else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
-      tmem_st8(a0col, a0.hi);
-      tmem_wait_st();
-    }
-    arrive_and_issue(0);
-  }
-  for (; tile < p.num_tiles; tile += npairs) {
-    const bool valid = I < p.end;
-    const uint64_t In = I + dI;
-    const bool has_next = tile + npairs < p.num_tiles;
-    float part = 0.0f;
-    for (uint32_t l = 0; l < p.NL; ++l) {
-      if (l + 1 == p.NL && p.NL > 1 && first && has_next) {  // next tile's A0 while the last layer runs
-        if (mode == MODE_PREDICT) {
-          make_a0_predict<PREC_BF16>(p, In < p.end ? In : p.begin, a0);
-        } else {
-          odometer_step_n<NG>(p.R, p.dD, D);
-          if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
+  if (warp == 9) {
+    // =========================== MMA issuer (leader) ===========================
+    if (leader) {
+      const uint32_t sb = smem_u32(smem);
+      const uint32_t idesc = p.idesc;  // M = 256, N = H/2
+      const uint64_t d_a0 = make_bdesc(sb + p.smem_a0, 256);
+      const uint64_t d_ones = make_bdesc(sb + p.smem_ones, 256);
+      const uint64_t d_b1 = make_bdesc(sb + p.off_b1, p.sbo_b1);
+      const uint64_t b1_half = (8ull * p.sbo_b1) >> 4;  // N-half b: 8 row groups further
+      const uint64_t bh_half = (8ull * p.sbo_bh) >> 4;
+      uint32_t ph_a0f = 0, ph_rf = 0, ph_db = 0, ph_aq = 0, region = 0, jt = ~0u;  // jt: tile round (trace)
+      for (uint64_t tile = pair; tile < p.num_tiles; tile += npairs) {
+        // layer 1 (K = 16, A0 from shared memory) into `region`
+        if (p.NL == 1 && tile != pair) {  // no hidden GEMM: the final layer's region is rewritten by layer 1
+          mbar_wait(&bars[PB_RF], ph_rf);
+          ph_rf ^= 1u;
         }
-        tmem_st8(a0col, a0.hi);
+        ++jt;
+        mbar_wait(&bars[PB_A0F], ph_a0f);
+        ph_a0f ^= 1u;
+        tc_fence_after();
+        if (lane == 0) trace_ev(p, 0, jt, 0);
+        {
+          const uint32_t d = tmem_base + region * H;
+          if (elect_one()) {
+            umma_f16_ss_pair(d, d_a0, d_b1, idesc, 0u);
+            umma_commit_pair(&bars[PB_DA]);
+            umma_f16_ss_pair(d + C::HALF, d_a0, d_b1 + b1_half, idesc, 0u);
+            umma_commit_pair(&bars[PB_DB]);
+            umma_commit_pair(&bars[PB_A0E]);
+          }
+          __syncwarp();
+          if (lane == 0) trace_ev(p, 0, jt, 11);
+        }
+        for (uint32_t l = 1; l < p.NL; ++l) {
+          const uint32_t src = tmem_base + region * H;  // packed A of layer l (in place)
+          region ^= 1u;
+          const uint32_t dst = tmem_base + region * H;
+          const uint64_t db = make_bdesc(sb + p.off_bh + (l - 1) * p.stride_bh, p.sbo_bh);
+          if (l == 1 && tile != pair) {  // the previous tile's final layer has read `dst`
+            mbar_wait(&bars[PB_RF], ph_rf);
+            ph_rf ^= 1u;
+          }
+          if (lane == 0) trace_ev(p, 0, jt, 1);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            mbar_wait(&bars[PB_AQ + j], ph_aq);
+            tc_fence_after();
+            if (lane == 0 && l <= 2) trace_ev(p, 0, jt, 2 + (l - 1) * 4 + j);
+            if (elect_one()) {
+              // quarter j = K [j QC, (j+1) QC): packed A columns of sub j/2, chunk j%2
+              const uint32_t acol = src + (j >> 1) * C::HALF + (j & 1) * (C::QC / 2);
+#pragma unroll
+              for (int s = 0; s < C::QSTEPS; ++s)
+                umma_f16_ts_pair(dst, acol + s * 8, db + (j * C::QSTEPS + s) * 16, idesc, (j | s) != 0);
+              if (j == 3) {
+                umma_f16_ss_pair(dst, d_ones, db + (H / 16) * 16, idesc, 1u);
+                umma_commit_pair(&bars[PB_DA]);
+              }
+#pragma unroll
+              for (int s = 0; s < C::QSTEPS; ++s)
+                umma_f16_ts_pair(dst + C::HALF, acol + s * 8, db + bh_half + (j * C::QSTEPS + s) * 16, idesc,
+                                 (j | s) != 0);
+              if (j == 3) {
+                umma_f16_ss_pair(dst + C::HALF, d_ones, db + bh_half + (H / 16) * 16, idesc, 1u);
+                umma_commit_pair(&bars[PB_DB]);
+              }
+            }
+            __syncwarp();
+          }
+          ph_aq ^= 1u;
+        }
+        // the last layer (reading the other region as A) completes before the
+        // next tile's layer 1 overwrites that region
+        ph_db ^= (p.NL - 1) & 1u;  // DB phases of the non-final layers
+        if (tile + npairs < p.num_tiles) mbar_wait(&bars[PB_DB], ph_db);
+        if (lane == 0) trace_ev(p, 0, jt, 10);
+        ph_db ^= 1u;
+        region ^= 1u;
       }
-      mbar_wait(&bars[2], phd);
-      phd ^= 1u;
-      tc_fence_after();
-      if (l + 1 < p.NL) {
-        // hidden epilogue: this sub's columns -> packed bf16 A (bias already in D)
+    }
+  } else if (warp == 8) {
+    // ============================ A0 producer ============================
+    // lane owns rows lane + 32 u (u = 0..3) of this CTA's 128 rows
+    uint64_t I0 = p.begin + pair * (2 * TILE_M) + rank * TILE_M + lane;
+    uint32_t D[4][MAXG];
+    if (mode != MODE_PREDICT) {
 #pragma unroll
-        for (int c = 0; c < C::CPS / 32; c += 2) {
-          uint32_t v[2][32];
-          tmem_ld32(dcol + c * 32, v[0]);
-          if (C::CPS / 32 > 1) tmem_ld32(dcol + (c + 1) * 32, v[1]);
-          tmem_wait_ld();
+      for (int u = 0; u < 4; ++u) init_digits_n<NG>(p.R, I0 + 32u * u, D[u]);
+    }
+    uint32_t ph_e = 0;
+    for (uint64_t tile = pair; tile < p.num_tiles; tile += npairs) {
+      if (tile != pair) {  // layer 1 of the previous tile has consumed the A0 tile
+        mbar_wait(&bars[PB_A0E], ph_e);
+        ph_e ^= 1u;
+      }
+      if (lane == 0) trace_ev(p, 3, (uint32_t)((tile - pair) / npairs), 0);
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && C::CPS / 32 == 1) break;
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              pk[j] = relu_bf16x2(__uint_as_float(v[u][2 * j]), __uint_as_float(v[u][2 * j + 1]));
-            tmem_st16(acol + (q * C::CPS + (c + u) * 32) / 2, pk);
-          }
+      for (int u = 0; u < 4; ++u) {
+        A0Regs a0;
+        const uint64_t I = I0 + 32u * u;
+        if (mode == MODE_PREDICT) {
+          make_a0_predict<PREC_BF16>(p, I < p.end ? I : p.begin, a0);
+        } else {
+          if (tile != pair) odometer_step_n<NG>(p.R, p.dD, D[u]);
+          if (SPG == 4) make_a0_sweep4(p, slut, D[u], a0); else make_a0_sweep<PREC_BF16>(p, slut, D[u], a0);
         }
-        tmem_wait_st();
-        arrive_and_issue(l + 1);
-      } else {
-        if (p.NL == 1 && first && has_next) {  // single hidden layer: L1 (reads A0) is done only now
-          if (mode == MODE_PREDICT) {
-            make_a0_predict<PREC_BF16>(p, In < p.end ? In : p.begin, a0);
-          } else {
-            odometer_step_n<NG>(p.R, p.dD, D);
-            if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
+        st_a0_smem(a0tile, lane + 32u * u, a0.hi);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&bars[PB_A0F], 0);
+      if (lane == 0) trace_ev(p, 3, (uint32_t)((tile - pair) / npairs), 1);
+      I0 += dI;
+    }
+  } else {
+    // ============================= epilogue =============================
+    const uint32_t q = warp >> 2;  // sub: output columns [q H/2, (q+1) H/2)
+    const bool last = q == C::NSUB - 1;
+    const uint32_t wq = warp & 3u;
+    const uint32_t row = wq * 32u + lane;
+    const uint32_t tl = (wq * 32u) << 16;
+    uint64_t* dbar = &bars[q ? PB_DB : PB_DA];
+    surr_record* mycand = ts.cand + (size_t)wq * CAND_CAP;
+    uint32_t ncand = 0, phd = 0, region = 0;
+    const float4* w4 = reinterpret_cast<const float4*>(smem + p.off_fin) + q * C::HALF / 4;
+    uint64_t I = p.begin + pair * (2 * TILE_M) + rank * TILE_M + row;
+    const bool tw = wq == 0 && lane == 0;  // trace writer of this sub
+    uint32_t jt = ~0u;
+    for (uint64_t tile = pair; tile < p.num_tiles; tile += npairs) {
+      ++jt;
+      const bool valid = I < p.end;
+      float part = 0.0f;
+      for (uint32_t l = 0; l < p.NL; ++l) {
+        const uint32_t dcol = tmem_base + tl + region * H + q * C::HALF;
+        region ^= 1u;
+        if (tw && l == 0) trace_ev(p, 1 + q, jt, 12);
+        mbar_wait(dbar, phd);
+        phd ^= 1u;
+        tc_fence_after();
+        if (tw && l < 3) trace_ev(p, 1 + q, jt, 3 * l);
+        if (l + 1 < p.NL) {
+          // two K quarters: ReLU + bf16 pack in place, then signal the issuer
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            uint32_t v[C::QC / 32][32];
+#pragma unroll
+            for (int c = 0; c < C::QC / 32; ++c) tmem_ld32(dcol + j * C::QC + c * 32, v[c]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < C::QC / 32; ++c) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                pk[i] = relu_bf16x2(__uint_as_float(v[c][2 * i]), __uint_as_float(v[c][2 * i + 1]));
+              tmem_st16(dcol + (j * C::QC + c * 32) / 2, pk);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(&bars[PB_AQ + 2 * q + j], 0);
+            if (tw && l < 2) trace_ev(p, 1 + q, jt, 3 * l + 1 + j);
           }
-          tmem_st8(a0col, a0.hi);
-        }
-        // final FP32 layer over this sub's columns: w relu(x) = (w/2) x + (w/2) |x|,
-        // w' in shared memory (broadcast loads); release D to the next tile first
-        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        const float4* w4 = reinterpret_cast<const float4*>(smem + p.off_fin) + q * C::CPS / 4;
+        } else {
+          // final FP32 layer over this sub's columns: w relu(x) = (w/2) x + (w/2) |x|
+          uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-        for (int c = 0; c < C::CPS / 32; c += 2) {
-          uint32_t v[2][32];
-          tmem_ld32(dcol + c * 32, v[0]);
-          if (C::CPS / 32 > 1) tmem_ld32(dcol + (c + 1) * 32, v[1]);
-          tmem_wait_ld();
-          if (c + 2 >= C::CPS / 32 && has_next) {
-            if (first) tmem_wait_st();   // next A0 stored
-            arrive_and_issue(0);         // next tile's layer 1: D fully read
-          }
+          for (int c = 0; c < C::HALF / 32; c += 2) {
+            uint32_t v[2][32];
+            tmem_ld32(dcol + c * 32, v[0]);
+            tmem_ld32(dcol + (c + 1) * 32, v[1]);
+            tmem_wait_ld();
+            if (c + 2 >= C::HALF / 32) {  // region read: the next tile's layer 2 may overwrite it
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_remote(&bars[PB_RF], 0);
+            }
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (u == 1 && C::CPS / 32 == 1) break;
+            for (int u = 0; u < 2; ++u) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 w = w4[((c + u) * 32 + j) / 4];
-              const float x0 = __uint_as_float(v[u][j]), x1 = __uint_as_float(v[u][j + 1]);
-              const float x2 = __uint_as_float(v[u][j + 2]), x3 = __uint_as_float(v[u][j + 3]);
-              acc[0] = ffma2(pack2(w.x, w.y), pack2(x0, x1), acc[0]);
-              acc[1] = ffma2(pack2(w.x, w.y), pack2(fabsf(x0), fabsf(x1)), acc[1]);
-              acc[2] = ffma2(pack2(w.z, w.w), pack2(x2, x3), acc[2]);
-              acc[3] = ffma2(pack2(w.z, w.w), pack2(fabsf(x2), fabsf(x3)), acc[3]);
+              for (int i = 0; i < 32; i += 4) {
+                const float4 w = w4[((c + u) * 32 + i) / 4];
+                const float x0 = __uint_as_float(v[u][i]), x1 = __uint_as_float(v[u][i + 1]);
+                const float x2 = __uint_as_float(v[u][i + 2]), x3 = __uint_as_float(v[u][i + 3]);
+                acc[0] = ffma2(pack2(w.x, w.y), pack2(x0, x1), acc[0]);
+                acc[1] = ffma2(pack2(w.x, w.y), pack2(fabsf(x0), fabsf(x1)), acc[1]);
+                acc[2] = ffma2(pack2(w.z, w.w), pack2(x2, x3), acc[2]);
+                acc[3] = ffma2(pack2(w.z, w.w), pack2(fabsf(x2), fabsf(x3)), acc[3]);
+              }
             }
           }
-        }
-        float a8[8];
+          float a8[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) unpack2(acc[j], a8[2 * j], a8[2 * j + 1]);
-        part = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+          for (int j = 0; j < 4; ++j) unpack2(acc[j], a8[2 * j], a8[2 * j + 1]);
+          part = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+          if (tw) trace_ev(p, 1 + q, jt, 9);
+        }
       }
-    }
-    float t = part;
-    if (C::NSUB > 1) {
-      if (!last) red[q * TILE_M + row] = part;
-      named_bar_sync(1, 128 * C::NSUB);
+      // sub 0's partial -> sub 1 through shared memory: barrier 1 = "written"
+      // (sub 0 arrives, sub 1 waits), barrier 2 = "consumed" (the reverse), so
+      // sub 0 never waits for sub 1's final layer
+      if (!last) {
+        if (tile != pair) named_bar_sync(2, 128 * C::NSUB);
+        red[row] = part;
+        named_bar_arrive(1, 128 * C::NSUB);
+      } else {
+        named_bar_sync(1, 128 * C::NSUB);
+      }
+      if (tw) trace_ev(p, 1 + q, jt, 10);
       if (last) {
-        float sum = 0.0f;
-#pragma unroll
-        for (int qq = 0; qq + 1 < C::NSUB; ++qq) sum += red[qq * TILE_M + row];
-        t = sum + part;
-      }
-      named_bar_sync(2, 128 * C::NSUB);  // partials consumed before the next tile overwrites them
-    }
-    if (last) {
-      t += p.c_out;
-      if (!ens_stage(p, valid, I, t)) {
-      } else if (mode == MODE_TOPK) {
-        const uint32_t key = f2key(t);
-        const bool pass = valid && key <= ts.misc[2];
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, pass);
-        if (m) {
-          const uint32_t n = __popc(m);
-          if (ncand + n > CAND_CAP) {
-            lock_acquire(ts, lane);
-            warp_merge(ts, mycand, ncand, p.k, lane);
-            lock_release(ts, lane);
-            ncand = 0;
-          }
-          if (pass) {
-            const uint32_t pos = ncand + __popc(m & ((1u << lane) - 1u));
-            mycand[pos].idx = I;
-            mycand[pos].key = key;
-            mycand[pos].pad = 0;
-          }
-          ncand += n;
-          __syncwarp();
+        float t = red[row] + part + p.c_out;
+        if (tile + npairs < p.num_tiles) named_bar_arrive(2, 128 * C::NSUB);
+        if (!ens_stage(p, valid, I, t)) {
+        } else if (mode == MODE_TOPK) {
+          topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
+        } else if (valid) {
+          p.t_dense[I - p.begin] = t;
         }
-      } else if (valid) {
-        p.t_dense[I - p.begin] = t;
       }
+      if (tw) trace_ev(p, 1 + q, jt, 11);
+      I += dI;
     }
-    I = In;
-  }
-  if (last && mode == MODE_TOPK && ncand) {
-    lock_acquire(ts, lane);
-    warp_merge(ts, mycand, ncand, p.k, lane);
-    lock_release(ts, lane);
+    if (last && mode == MODE_TOPK && ncand) {
+      lock_acquire(ts, lane);
+      warp_merge(ts, mycand, ncand, p.k, lane);
+      lock_release(ts, lane);
+    }
   }
 
   // ---- teardown
