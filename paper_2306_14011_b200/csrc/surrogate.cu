@@ -22,6 +22,9 @@
 #include "sweep_kernel3.cuh"
 #include "sweep_kernel5.cuh"
 #include "sweep_kernel_pair.cuh"
+#ifndef SURR_PAIR_NSUB
+#define SURR_PAIR_NSUB 2
+#endif
 
 using namespace surr;
 
@@ -149,10 +152,11 @@ struct KernelInfo {
 
 template <int H, int SPG>
 KernelInfo kinfo_pair() {
-  using C = CfgPair<H>;
-  KernelInfo ki{(const void*)&sweep_kernel_pair<H, SPG>, 1, C::THREADS, true};
+  constexpr int NS = SURR_PAIR_NSUB;
+  using C = CfgPair<H, NS>;
+  KernelInfo ki{(const void*)&sweep_kernel_pair<H, SPG, NS>, 1, C::THREADS, true};
   ki.a0_smem = true;
-  ki.red_bytes = TILE_M * 4;  // after the ones tile
+  ki.red_bytes = (NS - 1) * TILE_M * 4;  // after the ones tile
   ki.pair = true;
   return ki;
 }

@@ -30,23 +30,27 @@
 
 namespace surr {
 
-template <int H>
+template <int H, int NS>
 struct CfgPair {
-  static constexpr int NSUB = 2;
-  static constexpr int HALF = H / 2;       // N per half-MMA = columns per sub
+  static constexpr int NSUB = NS;          // epilogue warpgroups per CTA (column split)
+  static constexpr int HALF = H / 2;       // N per half-MMA
+  static constexpr int SUBC = H / NSUB;    // columns per sub
   static constexpr int QC = H / 4;         // columns per K quarter
+  static constexpr int QPS = 4 / NSUB;     // quarters per sub
   static constexpr int QSTEPS = QC / 16;   // UMMA K-steps per quarter
   static constexpr int TMEM_COLS = 512;
-  static constexpr int THREADS = 320;
+  static constexpr int EPI_WARPS = 4 * NSUB;
+  static constexpr int THREADS = 32 * EPI_WARPS + 64;  // + A0 producer + MMA issuer
   static_assert(2 * H <= 512 && H % 64 == 0, "two H-column regions");
+  static_assert(NSUB == 2 || NSUB == 4, "sub count");
 };
 
 enum { PB_LOAD = 0, PB_A0F = 1, PB_AQ = 2, PB_RF = 6, PB_DA = 7, PB_DB = 8, PB_A0E = 9 };
 
-template <int H, int SPG>
-__global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
+template <int H, int SPG, int NS>
+__global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
     sweep_kernel_pair(const __grid_constant__ KParams p, int mode) {
-  using C = CfgPair<H>;
+  using C = CfgPair<H, NS>;
   constexpr int NG = K0 / SPG;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5;
@@ -57,7 +61,7 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.smem_misc + 96);
   uint8_t* a0tile = smem + p.smem_a0;
-  float* red = reinterpret_cast<float*>(smem + p.smem_ones + 4096);  // [row] partial of sub 0
+  float* red = reinterpret_cast<float*>(smem + p.smem_ones + 4096);  // [sub][row] partials of subs < NSUB-1
   TopkShared ts;
   ts.lists = reinterpret_cast<surr_record*>(smem + p.smem_lists);
   ts.cand = reinterpret_cast<surr_record*>(smem + p.smem_cand);
@@ -69,7 +73,7 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
       mbar_init(&bars[PB_LOAD], 1);
       mbar_init(&bars[PB_A0F], 2);
       for (int j = 0; j < 4; ++j) mbar_init(&bars[PB_AQ + j], 8);
-      mbar_init(&bars[PB_RF], 16);
+      mbar_init(&bars[PB_RF], 2 * C::EPI_WARPS);
       mbar_init(&bars[PB_DA], 1);
       mbar_init(&bars[PB_DB], 1);
       mbar_init(&bars[PB_A0E], 1);
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
   const uint8_t* slut = smem + p.smem_lut;
   mbar_wait(&bars[PB_LOAD], 0);
 
-  if (warp == 9) {
+  if (warp == C::EPI_WARPS + 1) {
     // =========================== MMA issuer (leader) ===========================
     if (leader) {
       const uint32_t sb = smem_u32(smem);
@@ -163,8 +167,8 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
             tc_fence_after();
             if (lane == 0 && l <= 2) trace_ev(p, 0, jt, 2 + (l - 1) * 4 + j);
             if (elect_one()) {
-              // quarter j = K [j QC, (j+1) QC): packed A columns of sub j/2, chunk j%2
-              const uint32_t acol = src + (j >> 1) * C::HALF + (j & 1) * (C::QC / 2);
+              // quarter j = K [j QC, (j+1) QC): packed A columns of sub j/QPS, chunk j%QPS
+              const uint32_t acol = src + (j / C::QPS) * C::SUBC + (j % C::QPS) * (C::QC / 2);
 #pragma unroll
               for (int s = 0; s < C::QSTEPS; ++s)
                 umma_f16_ts_pair(dst, acol + s * 8, db + (j * C::QSTEPS + s) * 16, idesc, (j | s) != 0);
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
         region ^= 1u;
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == C::EPI_WARPS) {
     // ============================ A0 producer ============================
     // lane owns rows lane + 32 u (u = 0..3) of this CTA's 128 rows
     uint64_t I0 = p.begin + pair * (2 * TILE_M) + rank * TILE_M + lane;
@@ -230,34 +234,34 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
     }
   } else {
     // ============================= epilogue =============================
-    const uint32_t q = warp >> 2;  // sub: output columns [q H/2, (q+1) H/2)
+    const uint32_t q = warp >> 2;  // sub: output columns [q SUBC, (q+1) SUBC)
     const bool last = q == C::NSUB - 1;
     const uint32_t wq = warp & 3u;
     const uint32_t row = wq * 32u + lane;
     const uint32_t tl = (wq * 32u) << 16;
-    uint64_t* dbar = &bars[q ? PB_DB : PB_DA];
+    uint64_t* dbar = &bars[q * C::SUBC < C::HALF ? PB_DA : PB_DB];
     surr_record* mycand = ts.cand + (size_t)wq * CAND_CAP;
     uint32_t ncand = 0, phd = 0, region = 0;
-    const float4* w4 = reinterpret_cast<const float4*>(smem + p.off_fin) + q * C::HALF / 4;
+    const float4* w4 = reinterpret_cast<const float4*>(smem + p.off_fin) + q * C::SUBC / 4;
     uint64_t I = p.begin + pair * (2 * TILE_M) + rank * TILE_M + row;
-    const bool tw = wq == 0 && lane == 0;  // trace writer of this sub
+    const bool tw = wq == 0 && lane == 0 && (q == 0 || last);  // trace writers: first and last sub
     uint32_t jt = ~0u;
     for (uint64_t tile = pair; tile < p.num_tiles; tile += npairs) {
       ++jt;
       const bool valid = I < p.end;
       float part = 0.0f;
       for (uint32_t l = 0; l < p.NL; ++l) {
-        const uint32_t dcol = tmem_base + tl + region * H + q * C::HALF;
+        const uint32_t dcol = tmem_base + tl + region * H + q * C::SUBC;
         region ^= 1u;
-        if (tw && l == 0) trace_ev(p, 1 + q, jt, 12);
+        if (tw && l == 0) trace_ev(p, last ? 2 : 1, jt, 12);
         mbar_wait(dbar, phd);
         phd ^= 1u;
         tc_fence_after();
-        if (tw && l < 3) trace_ev(p, 1 + q, jt, 3 * l);
+        if (tw && l < 3) trace_ev(p, last ? 2 : 1, jt, 3 * l);
         if (l + 1 < p.NL) {
           // two K quarters: ReLU + bf16 pack in place, then signal the issuer
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < C::QPS; ++j) {
             uint32_t v[C::QC / 32][32];
 #pragma unroll
             for (int c = 0; c < C::QC / 32; ++c) tmem_ld32(dcol + j * C::QC + c * 32, v[c]);
@@ -273,19 +277,19 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_remote(&bars[PB_AQ + 2 * q + j], 0);
-            if (tw && l < 2) trace_ev(p, 1 + q, jt, 3 * l + 1 + j);
+            if (lane == 0) mbar_arrive_remote(&bars[PB_AQ + C::QPS * q + j], 0);
+            if (tw && l < 2) trace_ev(p, last ? 2 : 1, jt, 3 * l + 1 + j);
           }
         } else {
           // final FP32 layer over this sub's columns: w relu(x) = (w/2) x + (w/2) |x|
           uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-          for (int c = 0; c < C::HALF / 32; c += 2) {
+          for (int c = 0; c < C::SUBC / 32; c += 2) {
             uint32_t v[2][32];
             tmem_ld32(dcol + c * 32, v[0]);
             tmem_ld32(dcol + (c + 1) * 32, v[1]);
             tmem_wait_ld();
-            if (c + 2 >= C::HALF / 32) {  // region read: the next tile's layer 2 may overwrite it
+            if (c + 2 >= C::SUBC / 32) {  // region read: the next tile's layer 2 may overwrite it
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_remote(&bars[PB_RF], 0);
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) unpack2(acc[j], a8[2 * j], a8[2 * j + 1]);
           part = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
-          if (tw) trace_ev(p, 1 + q, jt, 9);
+          if (tw) trace_ev(p, last ? 2 : 1, jt, 9);
         }
       }
       // sub 0's partial -> sub 1 through shared memory: barrier 1 = "written"
@@ -316,14 +320,17 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
       // sub 0 never waits for sub 1's final layer
       if (!last) {
         if (tile != pair) named_bar_sync(2, 128 * C::NSUB);
-        red[row] = part;
+        red[q * TILE_M + row] = part;
         named_bar_arrive(1, 128 * C::NSUB);
       } else {
         named_bar_sync(1, 128 * C::NSUB);
       }
-      if (tw) trace_ev(p, 1 + q, jt, 10);
+      if (tw) trace_ev(p, last ? 2 : 1, jt, 10);
       if (last) {
-        float t = red[row] + part + p.c_out;
+        float t = part;
+#pragma unroll
+        for (int qq = C::NSUB - 2; qq >= 0; --qq) t += red[qq * TILE_M + row];
+        t += p.c_out;
         if (tile + npairs < p.num_tiles) named_bar_arrive(2, 128 * C::NSUB);
         if (!ens_stage(p, valid, I, t)) {
         } else if (mode == MODE_TOPK) {
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(CfgPair<H>::THREADS, 1)
           p.t_dense[I - p.begin] = t;
         }
       }
-      if (tw) trace_ev(p, 1 + q, jt, 11);
+      if (tw) trace_ev(p, last ? 2 : 1, jt, 11);
       I += dI;
     }
     if (last && mode == MODE_TOPK && ncand) {
