@@ -156,11 +156,15 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
           region ^= 1u;
           const uint32_t dst = tmem_base + region * H;
           const uint64_t db = make_bdesc(sb + p.off_bh + (l - 1) * p.stride_bh, p.sbo_bh);
-          if (l == 1 && tile != pair) {  // the previous tile's final layer has read `dst`
+          // NSUB = 2: the previous tile's final layer read `dst` before its subs'
+          // AQ arrivals for this layer (sub 0 -> half a, sub 1 -> half b), so no
+          // separate wait is needed; with 4 subs half a spans two subs
+          if (C::NSUB != 2 && l == 1 && tile != pair) {
             mbar_wait(&bars[PB_RF], ph_rf);
             ph_rf ^= 1u;
           }
           if (lane == 0) trace_ev(p, 0, jt, 1);
+          // N-half a streamed over the K quarters as their A columns arrive
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             mbar_wait(&bars[PB_AQ + j], ph_aq);
@@ -176,17 +180,24 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
                 umma_f16_ss_pair(dst, d_ones, db + (H / 16) * 16, idesc, 1u);
                 umma_commit_pair(&bars[PB_DA]);
               }
+            }
+            __syncwarp();
+          }
+          // N-half b in one chain (its output columns belong to the sub whose
+          // epilogue starts last; they are rewritten only after its AQ arrivals)
+          if (elect_one()) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t acol = src + (j / C::QPS) * C::SUBC + (j % C::QPS) * (C::QC / 2);
 #pragma unroll
               for (int s = 0; s < C::QSTEPS; ++s)
                 umma_f16_ts_pair(dst + C::HALF, acol + s * 8, db + bh_half + (j * C::QSTEPS + s) * 16, idesc,
                                  (j | s) != 0);
-              if (j == 3) {
-                umma_f16_ss_pair(dst + C::HALF, d_ones, db + bh_half + (H / 16) * 16, idesc, 1u);
-                umma_commit_pair(&bars[PB_DB]);
-              }
             }
-            __syncwarp();
+            umma_f16_ss_pair(dst + C::HALF, d_ones, db + bh_half + (H / 16) * 16, idesc, 1u);
+            umma_commit_pair(&bars[PB_DB]);
           }
+          __syncwarp();
           ph_aq ^= 1u;
         }
         // the last layer (reading the other region as A) completes before the
