@@ -91,14 +91,19 @@ struct KParams {
 static_assert(offsetof(KParams, fin_w) % 16 == 0 && offsetof(KParams, fin_nb) % 16 == 0,
               "epilogue constants must stay 16-byte aligned in the parameter bank (LDCU.128)");
 
+// Ensemble accumulator value of row I, loaded at the start of a tile so that
+// its latency is hidden behind the tile's MMAs (members e >= 1)
+__device__ __forceinline__ float ens_prefetch(const KParams& p, bool valid, uint64_t I) {
+  return (p.acc_mode >= 2 && valid) ? p.t_acc[I - p.acc_base] : 0.0f;
+}
 // Ensemble stage of one row's prediction; false = no output in this pass.
 // Uniform across a warp (depends on acc_mode only), so ballots stay legal.
-__device__ __forceinline__ bool ens_stage(const KParams& p, bool valid, uint64_t I, float& t) {
+__device__ __forceinline__ bool ens_stage(const KParams& p, bool valid, uint64_t I, float& t, float accp) {
   if (p.acc_mode == 0) return true;
   float* a = p.t_acc + (I - p.acc_base);
   if (p.acc_mode == 1) { if (valid) *a = t; return false; }
-  if (p.acc_mode == 2) { if (valid) *a += t; return false; }
-  t = ((valid ? *a : 0.0f) + t) * p.inv_e;  // members summed in order e = 0 .. E-1, mean in seconds
+  if (p.acc_mode == 2) { if (valid) *a = accp + t; return false; }
+  t = (accp + t) * p.inv_e;  // members summed in order e = 0 .. E-1, mean in seconds
   return true;
 }
 
@@ -507,6 +512,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
     }
     for (; tile < p.num_tiles; tile += p.dTiles) {
       const bool valid = I < p.end;
+    const float accp = ens_prefetch(p, valid, I);
       // ---------------- a2 + a3: A0 operand -> TMEM
       if (PREC == PREC_BF16) {
         tmem_st8(acol, a0.hi);
@@ -615,7 +621,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
       }
 
       // ---------------- outputs
-      if (!ens_stage(p, valid, I, t)) {
+      if (!ens_stage(p, valid, I, t, accp)) {
       } else if (mode == MODE_TOPK) {
         const uint32_t key = f2key(t);
         // conservative filter on the key alone (a stale read only admits extra

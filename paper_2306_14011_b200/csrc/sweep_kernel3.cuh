@@ -363,7 +363,9 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       t = pa + pb;
     }
     t += p.c_out;
-    if (!ens_stage(p, valid, I, t)) {
+    // (accumulator loaded here, not at the tile start: the 128-register budget
+    // of the 4-slot kernel has no room to carry it across the tile)
+    if (!ens_stage(p, valid, I, t, ens_prefetch(p, valid, I))) {
     } else if (mode == MODE_TOPK) {
       topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
     } else if (valid) {

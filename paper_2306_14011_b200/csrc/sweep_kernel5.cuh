@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
     const bool tr = q == 0 && wq == 0 && lane == 0;
     if (tr) trace_ev(p, s, jr, 0);
     const bool valid = I < p.end;
+    const float accp = ens_prefetch(p, valid, I);
     const uint64_t In = I + dI;
     const bool has_next = tile + p.dTiles < p.num_tiles;
     float part = 0.0f;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
 #pragma unroll
       for (int qq = 0; qq + 1 < C::NSUB; ++qq) t += red[(s * C::NSUB + qq) * TILE_M + row];
       t = t + part + p.c_out;
-      if (!ens_stage(p, valid, I, t)) {
+      if (!ens_stage(p, valid, I, t, accp)) {
       } else if (mode == MODE_TOPK) {
         const uint32_t key = f2key(t);
         const bool pass = valid && key <= ts.misc[2];

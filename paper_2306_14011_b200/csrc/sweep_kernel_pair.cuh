@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
     for (uint64_t tile = pair; tile < p.num_tiles; tile += npairs) {
       ++jt;
       const bool valid = I < p.end;
+    const float accp = ens_prefetch(p, valid, I);
       float part = 0.0f;
       for (uint32_t l = 0; l < p.NL; ++l) {
         const uint32_t dcol = tmem_base + tl + region * H + q * C::SUBC;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
         for (int qq = C::NSUB - 2; qq >= 0; --qq) t += red[qq * TILE_M + row];
         t += p.c_out;
         if (tile + npairs < p.num_tiles) named_bar_arrive(2, 128 * C::NSUB);
-        if (!ens_stage(p, valid, I, t)) {
+        if (!ens_stage(p, valid, I, t, accp)) {
         } else if (mode == MODE_TOPK) {
           topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
         } else if (valid) {
