@@ -197,8 +197,13 @@ def main():
     model = workloads.load_model(wl.weights)
     if wl.device_encoding:  # combined-training model: sweep for one target GPU (G3)
         model = workloads.with_device(model, workloads.device_features(wl.device_encoding, wl.devices[-1]))
-    N = int(np.prod([len(v) for v in vl]))
+    N_space = int(np.prod([len(v) for v in vl]))
+    # work of one step: the whole space, or a bounded window of it from |S|/3
+    # (the paper's 3.58e14-config space: the full-space time is projected)
+    N = wl.window or N_space
+    base = N_space // 3 if wl.window else 0
     lo, hi = shard_range(N, world, rank)
+    lo, hi = lo + base, hi + base
     h = pk.Surrogate(local).load(model, precision)
     k = wl.k
     dev = torch.device(f"cuda:{local}")
@@ -300,7 +305,8 @@ def main():
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": precision, "data": "synthetic",
-               "config": {"workload": wl.name, "space": f"{wl.space}: {N} configs",
+               "config": {"workload": wl.name, "space": f"{wl.space}: {N_space} configs"
+                          + (f", step = window [{base}, {base + N})" if wl.window else ""),
                           "net": "-".join(map(str, model["widths"])) + (f" x{members}" if members > 1 else ""),
                           "k": k, "precision": precision,
                           "weights": f"oracle-trained ({wl.weights})",
@@ -314,6 +320,8 @@ def main():
                             "k1_launches_per_step": k1_n / args.steps,
                             "flops_per_config": algorithmic_flops(model["widths"]) * members},
                "e2e": e2e, "gpu_launches": launches}
+        if wl.window:
+            out["config"]["full_space_seconds_projected"] = N_space / value
         with_clk = clk.summary()
         out["clocks"] = with_clk
         if not args.no_cpu_baseline and world == 1:

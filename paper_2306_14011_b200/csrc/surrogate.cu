@@ -234,8 +234,33 @@ surr_status check_device(surrogate* h, int dev) {
   return SURR_OK;
 }
 
+// dynamic shared-memory layout of one K1 launch (offsets into p); returns bytes
+size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_t k, int mode) {
+  const int nslot = ki.nslot;
+  size_t off = align_up(p.w_bytes, 128);
+  p.smem_lut = (uint32_t)off;
+  off = align_up(off + (mode == MODE_PREDICT ? 0 : lut_bytes), 128);
+  p.smem_lists = (uint32_t)off;
+  off += (mode == MODE_TOPK ? 2ull * k * sizeof(surr_record) : 0);
+  off = align_up(off, 128);
+  p.smem_cand = (uint32_t)off;
+  off += (mode == MODE_TOPK ? (size_t)nslot * 4 * CAND_CAP * sizeof(surr_record) : 0);  // last-sub warps
+  off = align_up(off, 128);
+  p.smem_misc = (uint32_t)off;
+  off += 256;
+  off = align_up(off, 1024);
+  p.smem_a0 = (uint32_t)off;
+  off += ki.a0_smem ? (size_t)nslot * 4096 : ki.red_bytes;
+  p.smem_ones = (uint32_t)off;
+  off += ki.a0_smem ? 4096 + ki.red_bytes : 0;
+  return off;
+}
+constexpr size_t SMEM_MAX = 227 * 1024;
+
 // ------------------------------------------------------------ space / LUT
-surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
+// k_hint: the top-k size the space is prepared for (shared-memory budget of the
+// 4-parameter decoder table)
+surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32_t k_hint = 1) {
   if (!sp || !sp->radix || !sp->values) return fail(h, SURR_E_INVALID_ARG, "null space descriptor");
   const uint32_t P = sp->num_params;
   if (P == 0 || P > SURR_MAX_PARAMS) return fail(h, SURR_E_INVALID_ARG, "num_params %u out of range", P);
@@ -259,20 +284,6 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
   h->sp.begin = sp->begin;
   h->sp.end = end;
   h->card = card;
-  if (!force && h->space_valid && radix == h->c_radix && values == h->c_values) return SURR_OK;
-
-  // super digits: group g holds A0 slots [spg g, spg (g+1)) (parameter j in slot j,
-  // the ones slot P carrying b_1, zeros after); R_g = product of its parameters'
-  // radices.  spg = 4 (8-byte entries = two packed bf16 columns) for the 3-slot
-  // BF16 kernel when the table fits in 64 KB, else 2.
-  const bool bf = h->prec == PREC_BF16;
-  KParams& k = h->sp;
-  std::vector<uint32_t> voff(P);
-  for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
-  auto slot_val = [&](uint32_t slot, uint32_t d) -> double {  // StandardScaler / min-max affine map
-    if (slot < P) return (values[voff[slot] + d] - h->hshift[slot]) / h->hscale[slot];
-    return slot == P ? 1.0 : 0.0;
-  };
   auto table_entries = [&](uint32_t spg_) {
     uint64_t e = 0;
     for (uint32_t g = 0; g < (uint32_t)K0 / spg_; ++g) {
@@ -282,8 +293,32 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
     }
     return e;
   };
+  // quadruples when the kernel takes them and a top-k launch still fits in
+  // shared memory with the larger table (e.g. the paper's 10/12-value lists:
+  // 2 x 14,400 + 2 x 120 + ... entries, 117 KB next to cfg2's 36 KB of weights)
   uint32_t spg = 2;
-  if (uses_quads(h->prec, h->H, h->NL) && table_entries(4) * 8 <= 64 * 1024) spg = 4;
+  if (uses_quads(h->prec, h->H, h->NL) && table_entries(4) * 8 <= 120 * 1024) {
+    KernelInfo ki4;
+    KParams tmp = h->mp;
+    if (get_kernel(h->prec, h->H, h->NL, &ki4, 4) &&
+        smem_layout(ki4, tmp, (uint32_t)align_up(table_entries(4) * 8, 16), std::max(k_hint, 1u), MODE_TOPK) <=
+            SMEM_MAX)
+      spg = 4;
+  }
+  if (!force && h->space_valid && radix == h->c_radix && values == h->c_values && spg == h->spg) return SURR_OK;
+
+  // super digits: group g holds A0 slots [spg g, spg (g+1)) (parameter j in slot j,
+  // the ones slot P carrying b_1, zeros after); R_g = product of its parameters'
+  // radices.  spg = 4: 8-byte entries = four packed bf16 columns (BF16 kernels
+  // with quadruple groups, see above), else 2.
+  const bool bf = h->prec == PREC_BF16;
+  KParams& k = h->sp;
+  std::vector<uint32_t> voff(P);
+  for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
+  auto slot_val = [&](uint32_t slot, uint32_t d) -> double {  // StandardScaler / min-max affine map
+    if (slot < P) return (values[voff[slot] + d] - h->hshift[slot]) / h->hscale[slot];
+    return slot == P ? 1.0 : 0.0;
+  };
   const uint32_t ng = K0 / spg;
   const size_t esz = bf ? 2 * spg : 16;  // bf16: spg packed halves; tf32 (spg 2): hi pair + lo pair
   size_t entries = 0;
@@ -295,7 +330,7 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force) {
     k.lut_off[g] = (uint32_t)entries;
     entries += g < ng ? r : 0;
   }
-  if (entries * esz > 96 * 1024) return fail(h, SURR_E_UNSUPPORTED, "value table too large (%zu entries)", entries);
+  if (entries * esz > 120 * 1024) return fail(h, SURR_E_UNSUPPORTED, "value table too large (%zu entries)", entries);
   std::vector<uint8_t> lut(align_up(entries * esz, 16), 0);
   for (uint32_t g = 0; g < ng; ++g) {
     for (uint32_t D = 0; D < k.R[g]; ++D) {
@@ -372,25 +407,8 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   p.dTiles = (uint32_t)(nslot * L->grid);
   if (mode != MODE_PREDICT) stride_digits(p.R, (uint64_t)p.dTiles * TILE_M, p.dD);
   p.k = mode == MODE_TOPK ? k : 1;
-  // dynamic shared memory layout
-  size_t off = align_up(p.w_bytes, 128);
-  p.smem_lut = (uint32_t)off;
-  off = align_up(off + (mode == MODE_PREDICT ? 0 : p.lut_bytes), 128);
-  p.smem_lists = (uint32_t)off;
-  off += (mode == MODE_TOPK ? 2ull * k * sizeof(surr_record) : 0);
-  off = align_up(off, 128);
-  p.smem_cand = (uint32_t)off;
-  off += (mode == MODE_TOPK ? (size_t)nslot * 4 * CAND_CAP * sizeof(surr_record) : 0);  // last-sub warps
-  off = align_up(off, 128);
-  p.smem_misc = (uint32_t)off;
-  off += 256;
-  off = align_up(off, 1024);
-  p.smem_a0 = (uint32_t)off;
-  off += L->ki.a0_smem ? (size_t)nslot * 4096 : L->ki.red_bytes;
-  p.smem_ones = (uint32_t)off;
-  off += L->ki.a0_smem ? 4096 + L->ki.red_bytes : 0;
-  L->smem = off;
-  if (L->smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "shared memory %zu B exceeds 227 KB", L->smem);
+  L->smem = smem_layout(L->ki, p, p.lut_bytes, k, mode);
+  if (L->smem > SMEM_MAX) return fail(h, SURR_E_UNSUPPORTED, "shared memory %zu B exceeds 227 KB", L->smem);
   L->p = p;
   return SURR_OK;
 }
@@ -523,7 +541,7 @@ surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint
   if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "no model loaded");
   if (k == 0 || k > SURR_K_MAX) return fail(h, SURR_E_INVALID_ARG, "k = %u outside 1..%u", k, SURR_K_MAX);
   CU(cudaSetDevice(h->dev));
-  surr_status rc = prepare_space(h, space, force);
+  surr_status rc = prepare_space(h, space, force, k);
   if (rc) return rc;
   const uint64_t begin = h->sp.begin, end = h->sp.end;
   const uint64_t n = end - begin;

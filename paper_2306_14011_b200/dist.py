@@ -57,3 +57,39 @@ def sweep(surrogate, value_lists, k: int, group=None):
         return idx, t
 
     return sweep_distributed(local, merge, n, k, group)
+
+
+def sweep_campaign(make_campaign, merge, n: int, k: int, group=None):
+    """Checkpointed multi-GPU sweep: each rank runs
+    ``make_campaign(lo, hi)`` (a `campaign.Campaign` over its shard, with its
+    own checkpoint file) to completion, then the per-rank records are exchanged
+    with one all_gather and merged as in `sweep_distributed`."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = shard_range(n, world, rank)
+    recs = make_campaign(lo, hi).run()
+    return merge(gather_records(recs, group), world, k)
+
+
+def campaign(surrogate, value_lists, k: int, chunk: int, ckpt_dir: str | None = None, tag: str = "",
+             every: int = 1, group=None):
+    """The product path of a checkpointed full-space sweep on every rank:
+    chunks of K1 + K2, K2 folds, per-rank checkpoint ``ckpt_dir/rank<r>.npz``,
+    one all_gather, K2 merge.  Returns (idx int64 [k], t float32 [k])."""
+    import os
+
+    import numpy as np
+
+    from . import campaign as cp
+    n = int(np.prod([len(v) for v in value_lists], dtype=object))
+    rank = dist.get_rank(group)
+
+    def make(lo, hi):
+        path = os.path.join(ckpt_dir, f"rank{rank}.npz") if ckpt_dir else None
+        return cp.for_surrogate(surrogate, value_lists, k, lo, hi, chunk, path, every, tag)
+
+    def merge(recs, world, kk):
+        idx, t, _ = surrogate.merge_topk(recs, world, kk, kk)
+        return idx, t
+
+    return sweep_campaign(make, merge, n, k, group)

@@ -256,3 +256,45 @@ def test_cfg3_full_sweep_reevaluated(pk):
     t = t.cpu().numpy()
     assert cnt == 64 and np.all(np.diff(t) >= 0)
     assert rel_err(t, osweep.times_at(model, vl, idx), model["y_scale"]).max() <= TOL["bf16"]
+
+
+# ------------------------------------------------------------------ the paper's space
+@pytest.mark.parametrize("b,n", [(358318080000000 - 300_001, 300_001), (123_456_789_012_345, (1 << 18) + 3)])
+def test_paper_space_window_times(pk, b, n):
+    # 10/12-value lists: quadruple decoder table of 117 KB, indices near 3.58e14
+    vl = workloads.space("paper")
+    model = workloads.load_model("paper_14-128-128-1")
+    h = _handle(pk, model, "bf16")
+    t = h.eval_range(vl, b, b + n).cpu().numpy()
+    ref = osweep.times(model, vl, b, b + n)
+    assert rel_err(t, ref, model["y_scale"]).max() <= TOL["bf16"]
+
+
+def test_paper_space_window_topk1024(pk):
+    vl = workloads.space("paper")
+    model = workloads.load_model("paper_14-128-128-1")
+    h = _handle(pk, model, "bf16")
+    b, e = 200_000_000_000_000, 200_000_000_000_000 + (1 << 20) + 17
+    idx, t, cnt = h.sweep(vl, 1024, b, e)
+    ri, rt = osweep.topk(model, vl, 1024, b, e)
+    assert cnt == 1024
+    check_topk(idx.cpu().numpy().astype(np.uint64), t.cpu().numpy(), ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL["bf16"], model["y_scale"])
+
+
+def test_campaign_chunked_and_resumed_equals_one_shot(pk, tmp_path):
+    from paper_2306_14011_b200 import campaign as cp
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, "bf16")
+    N = 170_859_375
+    full_i, full_t, _ = h.sweep(vl, 16)
+    path = str(tmp_path / "c.npz")
+    a = cp.for_surrogate(h, vl, 16, 0, N, 20_000_000, path, every=2, tag="cfg2/bf16")
+    a.run(max_chunks=5)
+    assert not a.finished
+    b = cp.for_surrogate(h, vl, 16, 0, N, 20_000_000, path, every=2, tag="cfg2/bf16")
+    assert b.resumed_from == 80_000_000
+    idx, t = cp.records_to_result(b.run().cpu().numpy(), 16)
+    assert np.array_equal(idx, full_i.cpu().numpy().astype(np.uint64))
+    assert np.array_equal(t, full_t.cpu().numpy())

@@ -66,6 +66,7 @@ class Workload:
     device_encoding: str | None = None   # None | "gflops" | "onehot"
     devices: list = field(default_factory=list)
     note: str = ""
+    window: int | None = None  # bench step = this many configs from |S|/3 (None: the whole space)
 
 
 # BASELINE.json configs (G5 for unstated widths).
@@ -83,6 +84,9 @@ WORKLOADS = {
                      note="combined-GPU-model variant: 14 params + one-hot GPU type, 8-member ensemble"),
     "cfg5": Workload("cfg5", "cfg5", [128, 128], 1024, "bf16", "cfg5_14-128-128-1", 10000,
                      note="large sweep 28^7 = 1.35e10 configs, top-1024 per rank"),
+    "paper": Workload("paper", "paper", [128, 128], 1024, "bf16", "paper_14-128-128-1", 10000, window=1 << 35,
+                      note="the paper's own space, 10^7 12^7 = 3.58e14 configs (P:241), top-1024; "
+                           "SURVEY 8(f) NEXT-2 (bench: a bounded index window, full-space time projected)"),
 }
 
 
