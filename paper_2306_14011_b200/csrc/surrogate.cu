@@ -43,8 +43,6 @@ struct surrogate {
   std::vector<KParams> members;  // per-member model parameters (ensemble)
   float* d_acc = nullptr;        // ensemble accumulation buffer (fp32 per config of a chunk)
   size_t d_acc_cap = 0;
-  double* d_zshift = nullptr;
-  double* d_zscale = nullptr;
   std::vector<double> hshift, hscale;  // host copies of the input affine map
   // space cache
   bool space_valid = false;
@@ -148,6 +146,7 @@ struct KernelInfo {
   bool a0_smem = false;  // SS-form A0 tiles + ones block in shared memory
   uint32_t red_bytes = 0;  // shared-memory partials of split-column epilogues
   bool pair = false;       // CTA-pair kernel (cluster of 2, cta_group::2, 256-row tiles)
+  bool x_stage = false;    // predict rows staged in shared memory by bulk copies
 };
 
 template <int H, int SPG>
@@ -181,6 +180,7 @@ KernelInfo kinfo3() {
   using C = Cfg3<H, NS>;
   KernelInfo ki{(const void*)&sweep_kernel3<H, SPG, NS>, C::NSLOT, C::THREADS, true};
   ki.a0_smem = C::A0_SMEM;
+  ki.x_stage = SPG == 0;  // the predict instantiation
   return ki;
 }
 
@@ -199,9 +199,13 @@ bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg 
   }
   // BF16 nets with at most one hidden->hidden layer: three tiles in flight
   if (uses_kernel3(prec, H, NL)) {
-    if (H == 32) { *ki = spg == 4 ? kinfo3<32, 4>() : kinfo3<32, 2>(); return true; }
-    if (H == 64) { *ki = spg == 4 ? kinfo3<64, 4>() : kinfo3<64, 2>(); return true; }
-    if (H == 128) { *ki = spg == 4 ? kinfo3<128, 4>() : kinfo3<128, 2>(); return true; }
+    // spg 0 = the predict instantiation
+    if (H == 32) { *ki = spg == 4 ? kinfo3<32, 4>() : spg == 2 ? kinfo3<32, 2>() : kinfo3<32, 0>(); return true; }
+    if (H == 64) { *ki = spg == 4 ? kinfo3<64, 4>() : spg == 2 ? kinfo3<64, 2>() : kinfo3<64, 0>(); return true; }
+    if (H == 128) {
+      *ki = spg == 4 ? kinfo3<128, 4>() : spg == 2 ? kinfo3<128, 2>() : kinfo3<128, 0>();
+      return true;
+    }
   }
   // FP32 (3xTF32) nets with at most one hidden->hidden layer: self-issuing, split
   // columns, separate D2 region (measured faster than the general kernel; for
@@ -253,6 +257,10 @@ size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_
   off += ki.a0_smem ? (size_t)nslot * 4096 : ki.red_bytes;
   p.smem_ones = (uint32_t)off;
   off += ki.a0_smem ? 4096 + ki.red_bytes : 0;
+  off = align_up(off, 128);
+  p.smem_x = (uint32_t)off;
+  p.x_tile_bytes = TILE_M * p.P * 4;  // a multiple of 16 (bulk-copy granule)
+  off += (mode == MODE_PREDICT && ki.x_stage) ? (size_t)nslot * p.x_tile_bytes : 0;
   return off;
 }
 constexpr size_t SMEM_MAX = 227 * 1024;
@@ -381,7 +389,8 @@ struct Launch {
 };
 
 surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L, uint32_t member = 0) {
-  if (!get_kernel(h->prec, h->H, h->NL, &L->ki, h->spg)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
+  if (!get_kernel(h->prec, h->H, h->NL, &L->ki, mode == MODE_PREDICT ? 0 : h->spg))
+    return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
   KParams p = h->members.empty() ? h->mp : h->members[member];
   const KParams& s = h->sp;
   if (mode != MODE_PREDICT) {
@@ -524,6 +533,8 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
       L.p.recs = h->d_recs + done * k;
       L.p.t_dense = t_dense ? t_dense + (c0 - begin) : nullptr;
       L.p.x = x;
+      // bulk copies need 16-byte aligned rows blocks: x itself, and c0 P 4 bytes
+      L.p.x_tma = (L.ki.x_stage && x && ((uintptr_t)x % 16) == 0 && (c0 * L.p.P * 4) % 16 == 0) ? 1u : 0u;
       L.p.trace = h->trace;
       L.p.trace_n = h->trace_n;
       rc = launch(h, L, m, st);
@@ -584,7 +595,7 @@ void surrogate_destroy(surrogate_t* h) {
   if (!h) return;
   cudaSetDevice(h->dev);
   cudaFree(h->d_w); cudaFree(h->d_lut); cudaFree(h->d_recs); cudaFree(h->d_merged);
-  cudaFree(h->d_zshift); cudaFree(h->d_zscale); cudaFree(h->d_acc);
+  cudaFree(h->d_acc);
   for (auto e : h->ev) cudaEventDestroy(e);
   delete h;
 }
@@ -767,17 +778,12 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     h->d_w_cap = img.size();
   }
   CU(cudaMemcpy(h->d_w, img.data(), img.size(), cudaMemcpyHostToDevice));
-  if (!h->d_zshift) {
-    if (cudaMalloc(&h->d_zshift, 32 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&h->d_zscale, 32 * sizeof(double)) != cudaSuccess)
-      return fail(h, SURR_E_OOM, "cudaMalloc");
-  }
-  CU(cudaMemcpy(h->d_zshift, shift.data(), P * sizeof(double), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(h->d_zscale, scale.data(), P * sizeof(double), cudaMemcpyHostToDevice));
   for (uint32_t e = 0; e < E; ++e) {
     mps[e].w_gmem = (const uint8_t*)h->d_w + e * wstride;
-    mps[e].zshift = h->d_zshift;
-    mps[e].zscale = h->d_zscale;
+    for (uint32_t j = 0; j < (uint32_t)K0; ++j) {  // predict prologue constants (parameter bank)
+      mps[e].zsh[j] = j < P ? shift[j] : 0.0;
+      mps[e].zinv[j] = j < P ? 1.0 / scale[j] : 0.0;
+    }
   }
   h->members.swap(mps);
   h->mp = h->members[0];

@@ -55,8 +55,8 @@ struct KParams {
   // predict rows
   const float* x;
   uint32_t P;
-  const double* zshift;      // [P]
-  const double* zscale;      // [P]
+  double zsh[K0];            // predict prologue: z_j = (x_j - zsh_j) * zinv_j (double,
+  double zinv[K0];           // parameter bank; zinv = 1 / scale, P:273 StandardScaler)
   // model
   uint32_t NL;               // UMMA layers (= number of hidden layers)
   const void* w_gmem;
@@ -77,6 +77,7 @@ struct KParams {
   float* t_dense;            // MODE_DENSE / MODE_PREDICT
   uint32_t smem_lut, smem_lists, smem_cand, smem_misc;  // byte offsets in dynamic smem
   uint32_t smem_a0, smem_ones;  // SS-form A0 tiles / ones block (4-slot kernel)
+  uint32_t smem_x, x_tile_bytes, x_tma;  // predict: per-slot staging of a tile's rows (bulk copy)
   // ensemble passes: acc_mode 0 = single net; 1 = first member,
   // t_acc[I - acc_base] = t; 2 = t_acc += t; 3 = last member, t = (t_acc + t) * inv_e
   float* t_acc;
@@ -323,28 +324,45 @@ __device__ __forceinline__ void make_a0_sweep4(const KParams& p, const uint8_t* 
   }
 }
 
-// explicit-batch rows: z_j = (x_j - shift_j) / scale_j in double (identical to
-// the host table), slot P = 1 (bias), rest 0
-template <int PREC>
-__device__ __forceinline__ void make_a0_predict(const KParams& p, uint64_t r, A0Regs& a) {
-  const float* xr = p.x + r * p.P;
-  float z[K0];
+// explicit-batch rows: z_j = (x_j - shift_j) * (1 / scale_j) in double (the host
+// table divides; the two agree to 1 ulp of double before the fp32 rounding),
+// slot P = 1 (bias), rest 0.  Column pairs are loaded (8-byte loads when P is
+// even) and converted one at a time to keep the live register set small.
+template <int PREC, bool SMEM = false>
+__device__ __forceinline__ void make_a0_row(const KParams& p, const float* xr, A0Regs& a) {
+  const bool even = (p.P & 1u) == 0;
+  // global rows: read-only path; staged rows: plain shared-memory loads
+  auto ld2 = [&](int j) { return SMEM ? *reinterpret_cast<const float2*>(xr + j) : __ldg(reinterpret_cast<const float2*>(xr + j)); };
+  auto ld1 = [&](int j) { return SMEM ? xr[j] : __ldg(xr + j); };
 #pragma unroll
-  for (int j = 0; j < K0; ++j) {
-    z[j] = 0.0f;
-    if (j < (int)p.P) z[j] = __double2float_rn(((double)__ldg(xr + j) - p.zshift[j]) / p.zscale[j]);
-    else if (j == (int)p.P) z[j] = 1.0f;
-  }
-  if (PREC == PREC_BF16) {
-#pragma unroll
-    for (int c = 0; c < K0 / 2; ++c) a.hi[c] = bf16x2(z[2 * c], z[2 * c + 1]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < K0; ++j) {
-      a.hi[j] = to_tf32(z[j]);
-      a.lo[j] = __float_as_uint(z[j] - __uint_as_float(a.hi[j]));  // exact; the UMMA truncates it to tf32
+  for (int j = 0; j < K0; j += 2) {
+    float x0 = 0.0f, x1 = 0.0f;
+    if (j + 1 < (int)p.P && even) {
+      const float2 v = ld2(j);
+      x0 = v.x;
+      x1 = v.y;
+    } else {
+      if (j < (int)p.P) x0 = ld1(j);
+      if (j + 1 < (int)p.P) x1 = ld1(j + 1);
+    }
+    float z0 = 0.0f, z1 = 0.0f;
+    if (j < (int)p.P) z0 = __double2float_rn(((double)x0 - p.zsh[j]) * p.zinv[j]);
+    else if (j == (int)p.P) z0 = 1.0f;
+    if (j + 1 < (int)p.P) z1 = __double2float_rn(((double)x1 - p.zsh[j + 1]) * p.zinv[j + 1]);
+    else if (j + 1 == (int)p.P) z1 = 1.0f;
+    if (PREC == PREC_BF16) {
+      a.hi[j / 2] = bf16x2(z0, z1);
+    } else {
+      a.hi[j] = to_tf32(z0);
+      a.lo[j] = __float_as_uint(z0 - __uint_as_float(a.hi[j]));  // exact; the UMMA truncates it to tf32
+      a.hi[j + 1] = to_tf32(z1);
+      a.lo[j + 1] = __float_as_uint(z1 - __uint_as_float(a.hi[j + 1]));
     }
   }
+}
+template <int PREC>
+__device__ __forceinline__ void make_a0_predict(const KParams& p, uint64_t r, A0Regs& a) {
+  make_a0_row<PREC>(p, p.x + r * p.P, a);
 }
 
 template <int PREC, int H>

@@ -147,7 +147,10 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     sweep_kernel3(const __grid_constant__ KParams p, int mode) {
   // SPG = parameter slots per decoder group: 4 (two A0 columns per 8-byte table
   // entry, 4 odometer digits) when the table fits, else 2 (8 digits)
-  constexpr int NG = K0 / SPG;
+  // SPG = 0: the explicit-batch (predict) instantiation, whose rows come from
+  // HBM; sweep instantiations carry no predict code (register budget)
+  constexpr bool PRED = SPG == 0;
+  constexpr int NG = PRED ? 1 : K0 / SPG;
   using C = Cfg3<H, NS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t warp = threadIdx.x >> 5;
@@ -165,6 +168,8 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     if (lane == 0) {
       mbar_init(&bars[0], 1);
       for (int s = 0; s < C::NSLOT; ++s) mbar_init(&bars[4 + s], 1);
+      if (PRED)
+        for (int s = 0; s < C::NSLOT; ++s) mbar_init(&bars[9 + s], 1);  // row staging (tmem_slot is at +64)
       fence_mbar_init();
       fence_proxy_async_smem();
       const uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
@@ -240,6 +245,30 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
   const uint64_t d_b2a = make_bdesc(sb + p.off_bh, p.sbo_bh);
   const uint64_t d_b2b = make_bdesc(sb + p.off_bh + (uint32_t)(H / 2 / 8) * p.sbo_bh, p.sbo_bh);
 
+  // predict: the rows of the slot's next tile are bulk-copied (TMA engine) into
+  // a per-slot shared-memory buffer one tile ahead; partial tiles, or an
+  // x pointer that is not 16-byte aligned, read global memory directly
+  uint8_t* xs = smem + p.smem_x + s * p.x_tile_bytes;
+  uint64_t* xbar = &bars[9 + s];
+  uint32_t phx = 0;
+  uint64_t x_next = 0;  // tile whose rows the next phase-0 issue prefetches
+  auto x_full = [&](uint64_t tl_) { return p.x_tma != 0u && p.begin + (tl_ + 1) * TILE_M <= p.end; };
+  auto x_issue = [&](uint64_t tl_) {  // one thread
+    if (tl_ < p.num_tiles && x_full(tl_)) {
+      mbar_arrive_expect_tx(xbar, p.x_tile_bytes);
+      bulk_g2s(xs, reinterpret_cast<const uint8_t*>(p.x + (p.begin + tl_ * TILE_M) * p.P), p.x_tile_bytes, xbar);
+    }
+  };
+  auto a0_pred = [&](uint64_t tl_, uint64_t I_, A0Regs& a) {
+    if (x_full(tl_)) {
+      mbar_wait(xbar, phx);
+      phx ^= 1u;
+      make_a0_row<PREC_BF16, true>(p, reinterpret_cast<const float*>(xs) + row * p.P, a);
+    } else {
+      make_a0_predict<PREC_BF16>(p, I_ < p.end ? I_ : p.begin, a);
+    }
+  };
+
   // every warp of the slot is done with its TMEM writes/reads -> issue one phase
   auto issue = [&](int phase) {
     tc_fence_before();
@@ -248,6 +277,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       tc_fence_after();
       if (elect_one()) {
         if (phase == 0) {
+          if (PRED) x_issue(x_next);  // the A0 tile holds the rows now: the buffer is free
           if (C::A0_SMEM) umma_f16_ss(dslot, d_a0, d_b1, idesc_full, 0u);
           else umma_f16_ts(dslot, tmem_base + C::A0_COL + 8 * s, d_b1, idesc_full, 0u);
         } else {
@@ -267,13 +297,16 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
   uint64_t I = p.begin + tile * TILE_M + row;
   const uint64_t dI = (uint64_t)p.dTiles * TILE_M;
   uint32_t D[MAXG];
-  if (mode != MODE_PREDICT) init_digits_n<NG>(p.R, I, D);
+  if (!PRED) init_digits_n<NG>(p.R, I, D);
   uint32_t phd = 0;
   mbar_wait(&bars[0], 0);
 
   A0Regs a0;
+  if (PRED && issuer && elect_one()) x_issue(tile);
+  __syncwarp();
+  x_next = tile + p.dTiles;
   if (tile < p.num_tiles) {
-    if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, I < p.end ? I : p.begin, a0);
+    if (PRED) a0_pred(tile, I, a0);
     else if (SPG == 4) make_a0_sweep4(p, slut, D, a0);
     else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
     put_a0(a0);
@@ -295,7 +328,10 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       tc_fence_after();
       t = final_partial<H>(p, dcol, 0);
       if (has_next) {
-        if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, In < p.end ? In : p.begin, a0);
+        if (PRED) {
+          a0_pred(tile + p.dTiles, In, a0);
+          x_next = tile + 2 * (uint64_t)p.dTiles;
+        }
         else {
           odometer_step_n<NG>(p.R, p.dD, D);
           if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
@@ -341,7 +377,10 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       if (tr) trace_ev(p, s, jr, 4);
       // ---- next tile's A0 while L2b runs (its 8-column area is idle now)
       if (has_next) {
-        if (mode == MODE_PREDICT) make_a0_predict<PREC_BF16>(p, In < p.end ? In : p.begin, a0);
+        if (PRED) {
+          a0_pred(tile + p.dTiles, In, a0);
+          x_next = tile + 2 * (uint64_t)p.dTiles;
+        }
         else {
           odometer_step_n<NG>(p.R, p.dD, D);
           if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
