@@ -35,6 +35,16 @@ def f32(x):
     return np.asarray(x, np.float32).astype(np.float64)
 
 
+def fp16(x):
+    return np.asarray(x, np.float32).astype(np.float16).astype(np.float64)
+
+
+def split_fp16(x):
+    hi = fp16(x)
+    lo = fp16(f32(x) - hi)
+    return hi, lo
+
+
 def split_tf32(x):
     hi = tf32(x)
     lo = tf32(f32(x) - hi)
@@ -56,6 +66,16 @@ def emulate(model, Z, mode, l1="bf16"):
                 d = f32(bf16(h) @ bf16(W[0]) + bf16(b[0]))
             else:
                 d = f32(f32(bf16(h) @ bf16(W[l])) + f32(b[l]))
+        elif mode == "fp16":
+            d = f32(f32(fp16(h) @ fp16(W[l])) + (fp16(b[l]) if l == 0 else f32(b[l])))
+        elif mode == "fp16x3":
+            hh, hl = split_fp16(h)
+            wh, wl = split_fp16(W[l])
+            if l == 0:
+                bh, bl = split_fp16(b[0])
+                d = f32(hh @ wh + hh @ wl + hl @ wh + bh + bl)
+            else:
+                d = f32(f32(hh @ wh + hh @ wl + hl @ wh) + f32(b[l]))
         else:
             hh, hl = split_tf32(h)
             wh, wl = split_tf32(W[l])
@@ -82,7 +102,7 @@ def main():
     Z = (X - model["x_shift"]) / model["x_scale"]
     t = oracle.sweep.times_at(model, vl, idx)
     den = np.maximum(np.abs(t), 1e-3 * model["y_scale"])
-    for mode, l1 in [("bf16", "bf16"), ("bf16", "bf16x3"), ("fp32", None)]:
+    for mode, l1 in [("bf16", "bf16"), ("bf16", "bf16x3"), ("fp16", None), ("fp16x3", None), ("fp32", None)]:
         te = emulate(model, Z, mode, l1)
         rel = np.abs(te - t) / den
         print(f"{name} {mode:5s} l1={l1}: max {rel.max():.3e}  p99.9 {np.quantile(rel, 0.999):.3e}"
