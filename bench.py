@@ -32,7 +32,11 @@ sys.path.insert(0, ROOT)
 
 import workloads  # noqa: E402
 
-PEAK_RATIO = {"bf16": 1.0, "tf32": 0.5, "fp32": 0.5}   # nominal dense tf32 / bf16 = 1.1 / 2.25 PF
+# nominal dense peak of the UMMA kind relative to bf16: kind::f16 (bf16 / fp16
+# operands) 1.0, kind::tf32 1.1 / 2.25 PF = 0.5
+PEAK_RATIO = {"f16": 1.0, "tf32": 0.5}
+# the arithmetic each precision runs as (the FP32 path: 3xFP16 where its kernel exists)
+DTYPE = {"bf16": "bf16", "fp16": "f16", "tf32": "tf32", "fp32_3xtf32": "3xtf32 (fp32 path)"}
 
 
 def algorithmic_flops(widths):
@@ -263,7 +267,10 @@ def main():
     # once a step is long enough for the power cap to act (>= 100 ms of K1)
     long_step = k1_step_s >= 0.1
     peak_kind = "sustained" if long_step else "burst"
-    peak = (sustained if long_step else burst) * PEAK_RATIO[precision]
+    mma_kind, passes, issued_per_config = h.arith()
+    ratio = PEAK_RATIO[mma_kind]
+    dtype = DTYPE.get(precision, f"3x{'fp16' if mma_kind == 'f16' else 'tf32'} (fp32 path)")
+    peak = (sustained if long_step else burst) * ratio
     traffic = ncu_traffic(wl.name, precision)
 
     # end to end through the public API: value table H2D + result D2H every step
@@ -309,7 +316,7 @@ def main():
         out = {"metric": "surrogate evals/sec over the 14-param space", "value": value, "unit": "evals/s",
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": precision, "data": "synthetic",
+               "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                "config": {"workload": wl.name, "space": f"{wl.space}: {N_space} configs"
                           + (f", step = window [{base}, {base + N})" if wl.window else ""),
                           "net": "-".join(map(str, model["widths"])) + (f" x{members}" if members > 1 else ""),
@@ -320,11 +327,15 @@ def main():
                           + ("" if collective else " [single process: no collective]")},
                "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": achieved / peak, "traffic": traffic,
-                            "peak_source": f"{src} bf16 {peak_kind} x {PEAK_RATIO[precision]} ({precision})",
-                            "frac_of_burst": achieved / (burst * PEAK_RATIO[precision]),
+                            "peak_source": f"{src} bf16 {peak_kind} x {ratio} (kind::{mma_kind}, {passes} pass(es))",
+                            "frac_of_burst": achieved / (burst * ratio),
                             "kernel": "sweep_kernel (K1)", "k1_ms_per_step": k1_step_s * 1e3,
                             "k1_launches_per_step": k1_n / args.steps,
-                            "flops_per_config": algorithmic_flops(model["widths"]) * members},
+                            "flops_per_config": algorithmic_flops(model["widths"]) * members,
+                            # what the tensor pipe executes (K padding, bias blocks, split passes)
+                            "issued_flops_per_config": issued_per_config * members,
+                            "issued_frac": achieved * issued_per_config * members
+                            / (algorithmic_flops(model["widths"]) * members) / peak},
                "e2e": e2e, "gpu_launches": launches}
         if wl.window:
             out["config"]["full_space_seconds_projected"] = N_space / value

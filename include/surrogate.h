@@ -52,7 +52,10 @@ typedef enum {
 typedef enum {
   SURR_PREC_BF16 = 0, /* BF16 operands, FP32 accumulate (tcgen05 kind::f16) */
   SURR_PREC_FP32 = 1, /* "FP32 path": 3xTF32 split (hi*hi + hi*lo + lo*hi), kind::tf32 */
-  SURR_PREC_TF32 = 2  /* 1xTF32 hidden layers, 3xTF32 first layer */
+  SURR_PREC_TF32 = 2, /* 1xTF32 hidden layers, 3xTF32 first layer */
+  SURR_PREC_FP16 = 3, /* IEEE FP16 operands, FP32 accumulate (kind::f16): BF16's tensor rate with
+                         11 significant bits instead of 8 (activations must stay below 65504) */
+  SURR_PREC_FP32_3XTF32 = 4 /* the FP32 path forced onto the 3xTF32 split */
 } surr_precision;
 
 #define SURR_K_MAX 1024u        /* largest top-k */
@@ -181,6 +184,16 @@ surr_status surrogate_reset_cache(surrogate_t *h);
 /* Bytes of the value lookup table of the cached space (the per-sweep H2D of
  * surrogate_sweep_host). */
 uint32_t surrogate_table_bytes(const surrogate_t *h);
+
+/* Tensor-core arithmetic the loaded model runs on: *mma_kind = 0 for
+ * tcgen05 kind::f16 (BF16 / FP16 operands), 1 for kind::tf32; *passes = UMMA
+ * passes per hidden-layer K step (1, or 3 for the split FP32 path: 3xFP16 or
+ * 3xTF32); *issued_flops = 2 x the MACs the sweep kernel issues to the tensor
+ * cores per config and ensemble member (K padding 14 -> 16, bias K blocks and
+ * split passes included; the FP32 final layer runs on CUDA cores).  The bench
+ * derives the roofline peak of the dtype and the issued rate from it.
+ * SURR_E_NOT_LOADED without a model. */
+surr_status surrogate_arith(const surrogate_t *h, uint32_t *mma_kind, uint32_t *passes, double *issued_flops);
 
 /* Number of kernel launches the last call issued on the GPU (for the bench's
  * gpu_launches count). */

@@ -16,7 +16,7 @@ import numpy as np
 
 from .build import LIB_PATH, build_library  # noqa: F401
 
-PREC = {"bf16": 0, "fp32": 1, "tf32": 2}
+PREC = {"bf16": 0, "fp32": 1, "tf32": 2, "fp16": 3, "fp32_3xtf32": 4}
 K_MAX = 1024
 EXPORTS = [
     "surrogate_create", "surrogate_destroy", "surrogate_last_error", "surrogate_load_weights",
@@ -24,6 +24,7 @@ EXPORTS = [
     "surrogate_merge_topk", "surrogate_sweep_records", "surrogate_decode_range", "surrogate_space_size",
     "surrogate_kernel_timing", "surrogate_kernel_timing_get", "surrogate_last_launches",
     "surrogate_selftest_umma", "surrogate_table_bytes", "surrogate_debug_trace", "surrogate_reset_cache",
+    "surrogate_arith",
 ]
 
 
@@ -79,6 +80,7 @@ def lib() -> ctypes.CDLL:
         L.surrogate_selftest_umma.argtypes = [i32, i32, u32, u32, vp, vp, vp]
         L.surrogate_debug_trace.argtypes = [vp, vp, u32]
         L.surrogate_reset_cache.argtypes = [vp]
+        L.surrogate_arith.argtypes = [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_double)]
         L.surrogate_table_bytes.argtypes = [vp]
         L.surrogate_table_bytes.restype = u32
         for name in EXPORTS:
@@ -239,6 +241,13 @@ class Surrogate:
     def reset_cache(self):
         """Drop the cached value table (next sweep rebuilds + uploads it)."""
         _check(lib().surrogate_reset_cache(self.h), self.h)
+
+    def arith(self):
+        """(mma kind, passes, issued tensor FLOPs per config and member) of the
+        loaded model's kernel: ("f16" | "tf32", 1 | 3, float)."""
+        kind, passes, fl = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_double()
+        _check(lib().surrogate_arith(self.h, ctypes.byref(kind), ctypes.byref(passes), ctypes.byref(fl)), self.h)
+        return ("f16" if kind.value == 0 else "tf32"), int(passes.value), float(fl.value)
 
     def lut_bytes(self) -> int:
         """Bytes of the value table uploaded by the last sweep (the per-step H2D)."""

@@ -180,6 +180,22 @@ __device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
   return d;
 }
+// the same for IEEE fp16 (SURR_PREC_FP16, and the hi / lo parts of 3xFP16)
+__device__ __forceinline__ uint32_t relu_f16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+__device__ __forceinline__ uint32_t f16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+// f16x2 -> the two floats it holds (exact)
+__device__ __forceinline__ void f16x2_to_f32(uint32_t v, float& lo, float& hi) {
+  asm("{\n .reg .f16 l, h;\n mov.b32 {l, h}, %2;\n cvt.f32.f16 %0, l;\n cvt.f32.f16 %1, h;\n}"
+      : "=f"(lo), "=f"(hi) : "r"(v));
+}
 // round to nearest even into tf32 (one F2FP.TF32; cvt.rna costs four SASS ops)
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t d;

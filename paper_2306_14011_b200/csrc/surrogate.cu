@@ -44,6 +44,11 @@ struct surrogate {
   float* d_acc = nullptr;        // ensemble accumulation buffer (fp32 per config of a chunk)
   size_t d_acc_cap = 0;
   std::vector<double> hshift, hscale;  // host copies of the input affine map
+  // FP16-operand precisions: per member, the layer-1 operand [W1; b1'] (K0 x H)
+  // and the hidden->hidden layers whose outputs feed another UMMA, for the
+  // range bound checked against each space (f16_range_check)
+  std::vector<std::vector<double>> rb_B1;
+  std::vector<std::vector<std::vector<double>>> rb_W, rb_b;
   // space cache
   bool space_valid = false;
   std::vector<uint32_t> c_radix;
@@ -99,6 +104,21 @@ uint16_t bf16_rne(float f) {  // same as __float2bfloat16_rn for finite values
   u += 0x7FFFu + ((u >> 16) & 1u);
   return (uint16_t)(u >> 16);
 }
+// IEEE binary16, round to nearest even, with subnormals (same as cvt.rn.f16.f32)
+uint16_t f16_rne(float f) {
+  const uint32_t u = f32_bits(f);
+  const uint16_t sign = (uint16_t)((u >> 16) & 0x8000u);
+  const uint32_t a = u & 0x7FFFFFFFu;
+  if (a > 0x7F800000u) return sign | 0x7E00u;
+  if (a >= 0x477FF000u) return sign | 0x7C00u;  // >= 65520 rounds to inf
+  if (a >= 0x38800000u) {                          // normal half (>= 2^-14)
+    const uint32_t r = (a + 0xFFFu + ((a >> 13) & 1u)) >> 13;
+    return sign | (uint16_t)(r - (112u << 10));
+  }
+  return sign | (uint16_t)std::nearbyint((double)bits_f32(a) * 16777216.0);  // multiples of 2^-24
+}
+// the 16-bit operand format of a kind::f16 precision
+uint16_t h16_rne(int prec, float f) { return prec == PREC_BF16 ? bf16_rne(f) : f16_rne(f); }
 uint32_t tf32_rn(float f) {  // same as cvt.rn.tf32.f32 (nearest even) for finite values
   uint32_t u = f32_bits(f);
   if ((u & 0x7FFFFFFFu) >= 0x7F800000u) return u;
@@ -109,6 +129,18 @@ void tf32_split(double x, uint32_t* hi, uint32_t* lo) {
   float f = (float)x;
   *hi = tf32_rn(f);
   *lo = f32_bits(f - bits_f32(*hi));
+}
+
+// hi = fp16(x), lo = fp16(x - hi) (3xFP16: 22 significant bits), from fp32(x)
+// as the kernel's explicit-batch prologue does (x - hi is exact in fp32)
+void f16_split(double xd, uint16_t* hi, uint16_t* lo) {
+  const float x = (float)xd;
+  *hi = f16_rne(x);
+  const uint32_t hb = *hi;  // decode the half exactly
+  const uint32_t ex = (hb >> 10) & 0x1Fu, man = hb & 0x3FFu;
+  double hv = ex ? std::ldexp(1024.0 + man, (int)ex - 25) : std::ldexp((double)man, -24);
+  if (hb & 0x8000u) hv = -hv;
+  *lo = f16_rne(x - (float)hv);
 }
 
 // K-major, no-swizzle UMMA operand image of an N x K matrix (element (n,k) =
@@ -147,13 +179,14 @@ struct KernelInfo {
   uint32_t red_bytes = 0;  // shared-memory partials of split-column epilogues
   bool pair = false;       // CTA-pair kernel (cluster of 2, cta_group::2, 256-row tiles)
   bool x_stage = false;    // predict rows staged in shared memory by bulk copies
+  uint32_t a0_tiles = 1;   // shared-memory A0 tiles per slot (3xFP16: hi + lo)
 };
 
-template <int H, int SPG>
+template <int H, int SPG, int PREC>
 KernelInfo kinfo_pair() {
   constexpr int NS = SURR_PAIR_NSUB;
   using C = CfgPair<H, NS>;
-  KernelInfo ki{(const void*)&sweep_kernel_pair<H, SPG, NS>, 1, C::THREADS, true};
+  KernelInfo ki{(const void*)&sweep_kernel_pair<H, SPG, NS, PREC>, 1, C::THREADS, true};
   ki.a0_smem = true;
   ki.red_bytes = (NS - 1) * TILE_M * 4;  // after the ones tile
   ki.pair = true;
@@ -165,6 +198,10 @@ KernelInfo kinfo5() {
   using C = Cfg5<PREC, H>;
   KernelInfo ki{(const void*)&sweep_kernel5<PREC, H>, C::NSLOT, C::THREADS, false};
   ki.red_bytes = C::NSLOT * C::NSUB * TILE_M * 4;
+  if (C::H16) {  // A0 hi / lo tiles in shared memory; partials after them
+    ki.a0_smem = true;
+    ki.a0_tiles = 2;
+  }
   return ki;
 }
 
@@ -174,52 +211,67 @@ KernelInfo kinfo() {
   return KernelInfo{(const void*)&sweep_kernel<PREC, H>, C::NSLOT, C::THREADS, C::BIAS_MMA};
 }
 
-template <int H, int SPG>
+template <int H, int SPG, int PREC>
 KernelInfo kinfo3() {
   constexpr int NS = 4;  // four 128-row tiles in flight per SM
   using C = Cfg3<H, NS>;
-  KernelInfo ki{(const void*)&sweep_kernel3<H, SPG, NS>, C::NSLOT, C::THREADS, true};
+  KernelInfo ki{(const void*)&sweep_kernel3<H, SPG, NS, PREC>, C::NSLOT, C::THREADS, true};
   ki.a0_smem = C::A0_SMEM;
   ki.x_stage = SPG == 0;  // the predict instantiation
   return ki;
 }
 
 bool uses_kernel3(int prec, uint32_t H, uint32_t NL) {
-  return prec == PREC_BF16 && NL <= 2 && (H == 32 || H == 64 || H == 128);
+  return is16(prec) && NL <= 2 && (H == 32 || H == 64 || H == 128);
 }
 bool uses_quads(int prec, uint32_t H, uint32_t NL) {  // kernels with 4-parameter decoder groups
-  return uses_kernel3(prec, H, NL) || (prec == PREC_BF16 && H == 256);
+  return uses_kernel3(prec, H, NL) || (is16(prec) && H == 256);
 }
 
-bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg = 2) {
-  // BF16 nets whose weights exceed one SM (H = 256): CTA pairs
-  if (prec == PREC_BF16 && H == 256) {
-    *ki = spg == 4 ? kinfo_pair<256, 4>() : kinfo_pair<256, 2>();
+template <int PREC>
+bool get_kernel16(uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg) {
+  // 16-bit nets whose weights exceed one SM (H = 256): CTA pairs
+  if (H == 256) {
+    *ki = spg == 4 ? kinfo_pair<256, 4, PREC>() : kinfo_pair<256, 2, PREC>();
     return true;
   }
-  // BF16 nets with at most one hidden->hidden layer: three tiles in flight
-  if (uses_kernel3(prec, H, NL)) {
+  // nets with at most one hidden->hidden layer: four tiles in flight
+  if (uses_kernel3(PREC, H, NL)) {
     // spg 0 = the predict instantiation
-    if (H == 32) { *ki = spg == 4 ? kinfo3<32, 4>() : spg == 2 ? kinfo3<32, 2>() : kinfo3<32, 0>(); return true; }
-    if (H == 64) { *ki = spg == 4 ? kinfo3<64, 4>() : spg == 2 ? kinfo3<64, 2>() : kinfo3<64, 0>(); return true; }
+    if (H == 32) {
+      *ki = spg == 4 ? kinfo3<32, 4, PREC>() : spg == 2 ? kinfo3<32, 2, PREC>() : kinfo3<32, 0, PREC>();
+      return true;
+    }
+    if (H == 64) {
+      *ki = spg == 4 ? kinfo3<64, 4, PREC>() : spg == 2 ? kinfo3<64, 2, PREC>() : kinfo3<64, 0, PREC>();
+      return true;
+    }
     if (H == 128) {
-      *ki = spg == 4 ? kinfo3<128, 4>() : spg == 2 ? kinfo3<128, 2>() : kinfo3<128, 0>();
+      *ki = spg == 4 ? kinfo3<128, 4, PREC>() : spg == 2 ? kinfo3<128, 2, PREC>() : kinfo3<128, 0, PREC>();
       return true;
     }
   }
+  return false;
+}
+
+bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg = 2) {
+  if (prec == PREC_BF16 && get_kernel16<PREC_BF16>(H, NL, ki, spg)) return true;
+  if (prec == PREC_FP16 && get_kernel16<PREC_FP16>(H, NL, ki, spg)) return true;
   // FP32 (3xTF32) nets with at most one hidden->hidden layer: self-issuing, split
   // columns, separate D2 region (measured faster than the general kernel; for
   // 1xTF32 the general two-slot kernel measured faster, 572 vs 482 TFLOP/s)
-  if (prec == PREC_FP32 && NL <= 2) {
+  if ((prec == PREC_FP32 || prec == PREC_FP32H) && NL <= 2) {
 #define CASE5(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo5<P_, H_>(); return true; }
     CASE5(PREC_FP32, 32) CASE5(PREC_FP32, 64) CASE5(PREC_FP32, 128)
+    CASE5(PREC_FP32H, 32) CASE5(PREC_FP32H, 64) CASE5(PREC_FP32H, 128)
     CASE5(PREC_TF32, 32) CASE5(PREC_TF32, 64) CASE5(PREC_TF32, 128)
 #undef CASE5
   }
 #define CASE(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo<P_, H_>(); return true; }
   CASE(PREC_BF16, 32) CASE(PREC_BF16, 64) CASE(PREC_BF16, 128)
+  CASE(PREC_FP16, 32) CASE(PREC_FP16, 64) CASE(PREC_FP16, 128)
   CASE(PREC_FP32, 32) CASE(PREC_FP32, 64) CASE(PREC_FP32, 128)
   CASE(PREC_TF32, 32) CASE(PREC_TF32, 64) CASE(PREC_TF32, 128)
 #undef CASE
@@ -254,7 +306,7 @@ size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_
   off += 256;
   off = align_up(off, 1024);
   p.smem_a0 = (uint32_t)off;
-  off += ki.a0_smem ? (size_t)nslot * 4096 : ki.red_bytes;
+  off += ki.a0_smem ? (size_t)nslot * ki.a0_tiles * 4096 : ki.red_bytes;
   p.smem_ones = (uint32_t)off;
   off += ki.a0_smem ? 4096 + ki.red_bytes : 0;
   off = align_up(off, 128);
@@ -266,6 +318,7 @@ size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_
 constexpr size_t SMEM_MAX = 227 * 1024;
 
 // ------------------------------------------------------------ space / LUT
+surr_status f16_range_check(surrogate* h, const std::vector<uint32_t>& radix, const std::vector<double>& values);
 // k_hint: the top-k size the space is prepared for (shared-memory budget of the
 // 4-parameter decoder table)
 surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32_t k_hint = 1) {
@@ -314,12 +367,14 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
       spg = 4;
   }
   if (!force && h->space_valid && radix == h->c_radix && values == h->c_values && spg == h->spg) return SURR_OK;
+  if (f16_range_check(h, radix, values) != SURR_OK) return SURR_E_RANGE;
 
   // super digits: group g holds A0 slots [spg g, spg (g+1)) (parameter j in slot j,
   // the ones slot P carrying b_1, zeros after); R_g = product of its parameters'
   // radices.  spg = 4: 8-byte entries = four packed bf16 columns (BF16 kernels
   // with quadruple groups, see above), else 2.
-  const bool bf = h->prec == PREC_BF16;
+  const bool bf = is16(h->prec);
+  const bool h3 = h->prec == PREC_FP32H;  // 3xFP16: fp16 hi pair + fp16 lo pair per entry
   KParams& k = h->sp;
   std::vector<uint32_t> voff(P);
   for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
@@ -328,7 +383,8 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
     return slot == P ? 1.0 : 0.0;
   };
   const uint32_t ng = K0 / spg;
-  const size_t esz = bf ? 2 * spg : 16;  // bf16: spg packed halves; tf32 (spg 2): hi pair + lo pair
+  // bf16 / fp16: spg packed halves; 3xFP16 (spg 2): fp16 hi pair + lo pair; tf32 (spg 2): hi pair + lo pair
+  const size_t esz = bf ? 2 * spg : h3 ? 8 : 16;
   size_t entries = 0;
   for (uint32_t g = 0; g < (uint32_t)MAXG; ++g) {
     uint64_t r = 1;
@@ -353,9 +409,14 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
       uint8_t* e = lut.data() + (k.lut_off[g] + (size_t)D) * esz;
       if (bf) {
         for (uint32_t q = 0; q < spg; ++q) {
-          const uint16_t v = bf16_rne((float)slot_val(spg * g + q, dig[q]));
+          const uint16_t v = h16_rne(h->prec, (float)slot_val(spg * g + q, dig[q]));
           memcpy(e + 2 * q, &v, 2);
         }
+      } else if (h3) {
+        uint16_t w[4];
+        f16_split(slot_val(2 * g, dig[0]), &w[0], &w[2]);
+        f16_split(slot_val(2 * g + 1, dig[1]), &w[1], &w[3]);
+        memcpy(e, w, 8);
       } else {
         uint32_t w[4];
         tf32_split(slot_val(2 * g, dig[0]), &w[0], &w[2]);
@@ -378,6 +439,53 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
   h->c_values = values;
   h->spg = spg;
   h->space_valid = true;
+  return SURR_OK;
+}
+
+// FP16 operands overflow above 65504.  Interval bound of every activation that
+// becomes a UMMA operand (z, and h_l = relu(W_l h_{l-1} + b_l) for l < NL) over
+// the space's value lists; SURR_E_RANGE if one can reach the FP16 limit.
+surr_status f16_range_check(surrogate* h, const std::vector<uint32_t>& radix, const std::vector<double>& values) {
+  if (h->prec != PREC_FP16 && h->prec != PREC_FP32H) return SURR_OK;
+  const uint32_t P = h->P, H = h->H;
+  const double LIM = 65504.0 * (1.0 - 1.0 / 2048.0);
+  std::vector<double> zlo(K0, 0.0), zhi(K0, 0.0);
+  for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) {
+    const double a = (values[o] - h->hshift[j]) / h->hscale[j];
+    const double b = (values[o + radix[j] - 1] - h->hshift[j]) / h->hscale[j];  // lists increase
+    zlo[j] = std::min(a, b);
+    zhi[j] = std::max(a, b);
+    if (std::max(std::fabs(a), std::fabs(b)) >= LIM)
+      return fail(h, SURR_E_RANGE, "normalised parameter %u reaches %g: outside the FP16 range", j,
+                  std::max(std::fabs(a), std::fabs(b)));
+  }
+  zlo[P] = zhi[P] = 1.0;  // ones slot (b_1)
+  double worst = 0.0;
+  for (size_t e = 0; e < h->rb_B1.size(); ++e) {
+    const std::vector<double>& B1 = h->rb_B1[e];
+    std::vector<double> U(H);
+    for (uint32_t n = 0; n < H; ++n) {
+      double u = 0.0;
+      for (uint32_t j = 0; j <= P; ++j) u += std::max(B1[(size_t)j * H + n] * zlo[j], B1[(size_t)j * H + n] * zhi[j]);
+      U[n] = std::max(0.0, u);
+    }
+    if (h->NL >= 2) worst = std::max(worst, *std::max_element(U.begin(), U.end()));
+    for (size_t l = 0; l < h->rb_W[e].size(); ++l) {
+      const std::vector<double>& W = h->rb_W[e][l];
+      std::vector<double> V(H);
+      for (uint32_t m = 0; m < H; ++m) {
+        double u = h->rb_b[e][l][m];
+        for (uint32_t n = 0; n < H; ++n) u += std::max(0.0, W[(size_t)n * H + m]) * U[n];
+        V[m] = std::max(0.0, u);
+      }
+      U.swap(V);
+      worst = std::max(worst, *std::max_element(U.begin(), U.end()));
+    }
+  }
+  if (worst >= LIM)
+    return fail(h, SURR_E_RANGE,
+                "hidden activations can reach %g over this space: outside the FP16 range (use BF16 or "
+                "SURR_PREC_FP32_3XTF32)", worst);
   return SURR_OK;
 }
 
@@ -604,6 +712,24 @@ const char* surrogate_last_error(const surrogate_t* h) { return h ? h->err.c_str
 
 uint32_t surrogate_last_launches(const surrogate_t* h) { return h ? h->launches : 0; }
 
+surr_status surrogate_arith(const surrogate_t* h, uint32_t* mma_kind, uint32_t* passes, double* issued_flops) {
+  if (!h || !mma_kind || !passes || !issued_flops) return SURR_E_INVALID_ARG;
+  if (!h->loaded) return SURR_E_NOT_LOADED;
+  KernelInfo ki;
+  if (!get_kernel(h->prec, h->H, h->NL, &ki)) return SURR_E_UNSUPPORTED;
+  const bool k16 = is16(h->prec) || h->prec == PREC_FP32H;
+  const bool split = h->prec == PREC_FP32 || h->prec == PREC_FP32H;
+  *mma_kind = k16 ? 0u : 1u;
+  *passes = split ? 3u : 1u;
+  const double H = h->H;
+  const double p1 = is16(h->prec) ? 1.0 : 3.0;                // layer 1 (K0 = 16)
+  const double kb = k16 ? 16.0 : 8.0;                         // bias K block
+  const double pb = split ? (k16 ? 1.0 : 2.0) : 1.0;
+  const double hidden = H * H * (*passes) + (ki.bias_mma ? kb * H * pb : 0.0);
+  *issued_flops = 2.0 * (K0 * H * p1 + (double)(h->NL - 1) * hidden);
+  return SURR_OK;
+}
+
 uint32_t surrogate_table_bytes(const surrogate_t* h) { return h && h->space_valid ? h->sp.lut_bytes : 0; }
 
 surr_status surrogate_space_size(const surr_space* sp, uint64_t* out) {
@@ -627,14 +753,16 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     return fail(h, SURR_E_UNSUPPORTED, "num_layers %u: need 1..%u hidden layers", L, SURR_MAX_HIDDEN_LAYERS);
   if (m->ensemble < 1 || m->ensemble > 64) return fail(h, SURR_E_INVALID_ARG, "ensemble %u outside 1..64", m->ensemble);
   const uint32_t E = m->ensemble;
-  if (m->precision != SURR_PREC_BF16 && m->precision != SURR_PREC_FP32 && m->precision != SURR_PREC_TF32)
+  if (m->precision != SURR_PREC_BF16 && m->precision != SURR_PREC_FP32 && m->precision != SURR_PREC_TF32 &&
+      m->precision != SURR_PREC_FP16 && m->precision != SURR_PREC_FP32_3XTF32)
     return fail(h, SURR_E_INVALID_ARG, "precision %d", (int)m->precision);
+  const bool p16 = m->precision == SURR_PREC_BF16 || m->precision == SURR_PREC_FP16;
   const uint32_t F = m->widths[0], H = m->widths[1];
   if (m->widths[L] != 1) return fail(h, SURR_E_INVALID_ARG, "output width must be 1");
   for (uint32_t l = 1; l < L; ++l)
     if (m->widths[l] != H) return fail(h, SURR_E_UNSUPPORTED, "hidden widths must be equal");
-  if (H != 32 && H != 64 && H != 128 && !(H == 256 && m->precision == SURR_PREC_BF16))
-    return fail(h, SURR_E_UNSUPPORTED, "hidden width %u not in {32,64,128} (256: BF16 only)", H);
+  if (H != 32 && H != 64 && H != 128 && !(H == 256 && p16))
+    return fail(h, SURR_E_UNSUPPORTED, "hidden width %u not in {32,64,128} (256: BF16 / FP16 only)", H);
   if (m->num_const_features > F || (m->num_const_features && !m->const_features))
     return fail(h, SURR_E_INVALID_ARG, "const features");
   const uint32_t P = F - m->num_const_features;
@@ -643,7 +771,14 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     if (!m->W[l] || !m->b[l]) return fail(h, SURR_E_INVALID_ARG, "null layer %u", l);
   CU(cudaSetDevice(h->dev));
 
-  const int prec = m->precision == SURR_PREC_BF16 ? PREC_BF16 : m->precision == SURR_PREC_FP32 ? PREC_FP32 : PREC_TF32;
+  // the FP32 path runs as 3xFP16 where its kernel exists (H <= 128, <= 2 hidden
+  // layers: twice the tensor rate of 3xTF32, the same 22 significant bits),
+  // else (or when forced) as 3xTF32
+  const int prec = m->precision == SURR_PREC_BF16   ? PREC_BF16
+                   : m->precision == SURR_PREC_FP16 ? PREC_FP16
+                   : m->precision == SURR_PREC_TF32 ? PREC_TF32
+                   : m->precision == SURR_PREC_FP32 && L - 1 <= 2 && H <= 128 ? PREC_FP32H
+                                                    : PREC_FP32;
   const uint32_t NL = L - 1;
   std::vector<double> shift(F), scale(F);
   for (uint32_t j = 0; j < F; ++j) {
@@ -652,6 +787,8 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   }
   std::vector<KParams> mps(E);
   std::vector<std::vector<uint8_t>> imgs(E);
+  std::vector<std::vector<double>> rb_B1(E);
+  std::vector<std::vector<std::vector<double>>> rb_W(E), rb_b(E);
   for (uint32_t e = 0; e < E; ++e) {
     // layer 1 operand rows: z_0..z_{P-1}, ones slot carrying b_1 + W1[const] z_const, zeros
     const double* W1 = m->W[e * L + 0];
@@ -666,15 +803,30 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
       }
       B1[(size_t)P * H + n] = b;
     }
-    const bool bf = prec == PREC_BF16;
+    rb_B1[e] = B1;
+    for (uint32_t l = 1; l + 1 < NL; ++l) {  // hidden->hidden layers feeding another UMMA
+      rb_W[e].emplace_back(m->W[e * L + l], m->W[e * L + l] + (size_t)H * H);
+      rb_b[e].emplace_back(m->b[e * L + l], m->b[e * L + l] + H);
+    }
+    if (prec == PREC_FP16 || prec == PREC_FP32H) {
+      double wmax = 0.0;
+      for (double x : B1) wmax = std::max(wmax, std::fabs(x));
+      for (uint32_t l = 1; l < NL; ++l)
+        for (size_t i = 0; i < (size_t)H * H; ++i) wmax = std::max(wmax, std::fabs(m->W[e * L + l][i]));
+      for (uint32_t l = 1; l < NL; ++l)
+        for (uint32_t i = 0; i < H; ++i) wmax = std::max(wmax, std::fabs(m->b[e * L + l][i]));
+      if (wmax >= 65504.0 * (1.0 - 1.0 / 2048.0))
+        return fail(h, SURR_E_RANGE, "weight magnitude %g outside the FP16 range", wmax);
+    }
+    const bool bf = is16(prec) || prec == PREC_FP32H;  // 16-bit operand image
     const uint32_t esz = bf ? 2 : 4;
     KernelInfo ki;
     if (!get_kernel(prec, H, L - 1, &ki)) return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", H);
     const bool bias_mma = ki.bias_mma;     // hidden biases as an extra UMMA K block
     const uint32_t kstep = bf ? 16 : 8;
     const uint32_t KH = H + (bias_mma ? kstep : 0);  // K extent of a hidden-layer B image
-    const bool lo1 = !bf;                  // layer 1 carries a lo part in both TF32 modes
-    const bool loh = prec == PREC_FP32;    // hidden layers carry a lo part (3xTF32)
+    const bool lo1 = !is16(prec);          // layer 1 carries a lo part (TF32 modes, 3xFP16)
+    const bool loh = prec == PREC_FP32 || prec == PREC_FP32H;  // hidden layers carry a lo part
     // CTA-pair kernel: rank r's image holds B columns [r NR, (r+1) NR) of every layer
     const uint32_t ranks = ki.pair ? 2 : 1;
     const uint32_t NR = H / ranks;
@@ -715,8 +867,13 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
           if (kk < Ksrc) x = src[(size_t)kk * N + n];
           else if (kk == Ksrc && bias) x = bias[n];
           const size_t o = pack_offset(nl, kk, K, esz);
-          if (bf) {
-            uint16_t v = bf16_rne((float)x);
+          if (bf && lo_part) {
+            uint16_t hi, lo;
+            f16_split(x, &hi, &lo);
+            memcpy(&img[base + o], &hi, 2);
+            memcpy(&img[lo_base + o], &lo, 2);
+          } else if (bf) {
+            uint16_t v = h16_rne(prec, (float)x);
             memcpy(&img[base + o], &v, 2);
           } else {
             uint32_t hi, lo;
@@ -761,7 +918,9 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     p.NL = NL;
     p.sbo_b1 = (K0 / (16 / esz)) * 128;
     p.sbo_bh = (KH / (16 / esz)) * 128;
-    p.idesc = ki.pair ? make_idesc(1, H / 2, 2 * TILE_M) : make_idesc(bf ? 1 : 2, H, TILE_M);
+    // a/b format: kind::f16 F16 = 0, BF16 = 1; kind::tf32 TF32 = 2
+    const int fmt = prec == PREC_BF16 ? 1 : (prec == PREC_FP16 || prec == PREC_FP32H) ? 0 : 2;
+    p.idesc = ki.pair ? make_idesc(fmt, H / 2, 2 * TILE_M) : make_idesc(fmt, H, TILE_M);
     p.P = P;
     mps[e] = p;
     imgs[e].swap(img);
@@ -786,6 +945,9 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     }
   }
   h->members.swap(mps);
+  h->rb_B1.swap(rb_B1);
+  h->rb_W.swap(rb_W);
+  h->rb_b.swap(rb_b);
   h->mp = h->members[0];
   h->hshift = shift;
   h->hscale = scale;

@@ -32,7 +32,23 @@
 
 namespace surr {
 
-enum { PREC_BF16 = 0, PREC_FP32 = 1, PREC_TF32 = 2 };
+// PREC_FP32 = 3xTF32, PREC_FP32H = 3xFP16 (both the "FP32 path"); PREC_FP16 =
+// 1xFP16 hidden layers (same tensor rate as BF16, 3 more mantissa bits)
+enum { PREC_BF16 = 0, PREC_FP32 = 1, PREC_TF32 = 2, PREC_FP16 = 3, PREC_FP32H = 4 };
+// 16-bit operand kernels (kind::f16): one element per half column
+__host__ __device__ constexpr bool is16(int prec) { return prec == PREC_BF16 || prec == PREC_FP16; }
+// relu + pack / pack a column pair into the precision's 16-bit operand format
+template <int PREC>
+__device__ __forceinline__ uint32_t relu_pk16(float lo, float hi) {
+  return PREC == PREC_FP16 ? relu_f16x2(lo, hi) : relu_bf16x2(lo, hi);
+}
+template <int PREC>
+__device__ __forceinline__ uint32_t pk16(float lo, float hi) {
+  return PREC == PREC_FP16 ? f16x2(lo, hi) : bf16x2(lo, hi);
+}
+// 1.0 in the precision's 16-bit format (K slot 0 of the bias ones block)
+template <int PREC>
+__host__ __device__ constexpr uint32_t one16() { return PREC == PREC_FP16 ? 0x3C00u : 0x3F80u; }
 enum { MODE_TOPK = 0, MODE_DENSE = 1, MODE_PREDICT = 2 };
 
 constexpr int MAXG = 8;       // super-digit groups = A0 column pairs (K0 / 2)
@@ -121,7 +137,7 @@ __device__ __forceinline__ void trace_ev(const KParams& p, uint32_t s, uint32_t 
 
 template <int PREC, int H>
 struct Cfg {
-  static constexpr int A_COLS = PREC == PREC_BF16 ? H / 2 : (PREC == PREC_FP32 ? 2 * H : H);
+  static constexpr int A_COLS = is16(PREC) ? H / 2 : (PREC == PREC_FP32 ? 2 * H : H);
   static constexpr int SLOT_COLS = H + A_COLS;
   static constexpr int NSLOT = (2 * SLOT_COLS <= 512) ? 2 : 1;
   // hidden-layer biases as an extra UMMA K block against a shared ones block
@@ -131,8 +147,8 @@ struct Cfg {
   static constexpr int TMEM_COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr int THREADS = 128 * (1 + NSLOT);
   static constexpr int PASSES_H = PREC == PREC_FP32 ? 3 : 1;   // hidden layers
-  static constexpr int PASSES_1 = PREC == PREC_BF16 ? 1 : 3;   // layer 1
-  static constexpr int KSTEP = PREC == PREC_BF16 ? 16 : 8;     // K per UMMA
+  static constexpr int PASSES_1 = is16(PREC) ? 1 : 3;   // layer 1
+  static constexpr int KSTEP = is16(PREC) ? 16 : 8;     // K per UMMA
   // A0 lo-part column offset (tf32 modes): fp32 keeps lo next to the hidden lo region
   static constexpr int A0_LO = PREC == PREC_FP32 ? H : K0;
   static_assert(NEED <= 512, "TMEM budget");
@@ -293,7 +309,8 @@ __device__ __forceinline__ void lock_release(TopkShared& ts, uint32_t lane) {
 }
 
 
-// A0 operand of one row: bf16 -> 8 packed columns; tf32 -> 16 hi + 16 lo slots.
+// A0 operand of one row: bf16 / fp16 -> 8 packed columns; 3xFP16 -> 8 hi + 8 lo
+// packed columns; tf32 -> 16 hi + 16 lo slots.
 struct A0Regs {
   uint32_t hi[K0], lo[K0];
 };
@@ -304,8 +321,12 @@ __device__ __forceinline__ void make_a0_sweep(const KParams& p, const uint8_t* s
                                               A0Regs& a) {
 #pragma unroll
   for (int g = 0; g < MAXG; ++g) {
-    if (PREC == PREC_BF16) {
+    if (is16(PREC)) {
       a.hi[g] = reinterpret_cast<const uint32_t*>(slut)[p.lut_off[g] + D[g]];
+    } else if (PREC == PREC_FP32H) {  // 8-byte entry: fp16 hi pair, fp16 lo pair
+      const uint2 e = reinterpret_cast<const uint2*>(slut)[p.lut_off[g] + D[g]];
+      a.hi[g] = e.x;
+      a.lo[g] = e.y;
     } else {
       const uint4 e = reinterpret_cast<const uint4*>(slut)[p.lut_off[g] + D[g]];
       a.hi[2 * g] = e.x; a.hi[2 * g + 1] = e.y; a.lo[2 * g] = e.z; a.lo[2 * g + 1] = e.w;
@@ -350,8 +371,13 @@ __device__ __forceinline__ void make_a0_row(const KParams& p, const float* xr, A
     else if (j == (int)p.P) z0 = 1.0f;
     if (j + 1 < (int)p.P) z1 = __double2float_rn(((double)x1 - p.zsh[j + 1]) * p.zinv[j + 1]);
     else if (j + 1 == (int)p.P) z1 = 1.0f;
-    if (PREC == PREC_BF16) {
-      a.hi[j / 2] = bf16x2(z0, z1);
+    if (is16(PREC)) {
+      a.hi[j / 2] = pk16<PREC>(z0, z1);
+    } else if (PREC == PREC_FP32H) {  // fp16 hi + fp16(z - hi) lo
+      a.hi[j / 2] = f16x2(z0, z1);
+      float h0, h1;
+      f16x2_to_f32(a.hi[j / 2], h0, h1);
+      a.lo[j / 2] = f16x2(z0 - h0, z1 - h1);
     } else {
       a.hi[j] = to_tf32(z0);
       a.lo[j] = __float_as_uint(z0 - __uint_as_float(a.hi[j]));  // exact; the UMMA truncates it to tf32
@@ -418,7 +444,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
     uint32_t ones[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) ones[j] = 0u;
-    ones[0] = PREC == PREC_BF16 ? 0x00003F80u : 0x3F800000u;
+    ones[0] = is16(PREC) ? one16<PREC>() : 0x3F800000u;
     tmem_st8(tmem_base + (((warp & 3u) * 32u) << 16) + C::ONES_COL, ones);
     tmem_wait_st();
   }
@@ -464,7 +490,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
               // K0 = 16: one bf16 step, or two tf32 steps x 3 passes
 #pragma unroll
               for (int kk = 0; kk < K0 / C::KSTEP; ++kk) {
-                if (PREC == PREC_BF16) {
+                if (is16(PREC)) {
                   umma_f16_ts(d, a + kk * 8, d_b1 + kk * 16, idesc, kk > 0);
                 } else {
                   umma_tf32_ts(d, a + kk * 8, d_b1 + kk * 16, idesc, kk > 0);
@@ -475,7 +501,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
             } else {
 #pragma unroll
               for (int kk = 0; kk < H / C::KSTEP; ++kk) {
-                if (PREC == PREC_BF16) {
+                if (is16(PREC)) {
                   umma_f16_ts(d, a + kk * 8, d_bh + kk * 16, idesc, kk > 0);
                 } else {
                   umma_tf32_ts(d, a + kk * 8, d_bh + kk * 16, idesc, kk > 0);
@@ -487,7 +513,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
               }
               if (C::BIAS_MMA) {  // D += ones * [b; 0] (the B image carries one extra K block)
                 constexpr int kb = H / C::KSTEP;
-                if (PREC == PREC_BF16) {
+                if (is16(PREC)) {
                   umma_f16_ts(d, ones, d_bh + kb * 16, idesc, 1u);
                 } else {
                   umma_tf32_ts(d, ones, d_bh + kb * 16, idesc, 1u);
@@ -532,7 +558,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
       const bool valid = I < p.end;
     const float accp = ens_prefetch(p, valid, I);
       // ---------------- a2 + a3: A0 operand -> TMEM
-      if (PREC == PREC_BF16) {
+      if (is16(PREC)) {
         tmem_st8(acol, a0.hi);
       } else {
         tmem_st16(acol, a0.hi);
@@ -577,11 +603,11 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
                 for (int j = 0; j < 32; ++j)
                   v[u][j] = __float_as_uint(__uint_as_float(v[u][j]) + p.hbias[(l - 1) & 1][cc * 32 + j]);
               }
-              if (PREC == PREC_BF16) {
+              if (is16(PREC)) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
-                  pk[j] = relu_bf16x2(__uint_as_float(v[u][2 * j]), __uint_as_float(v[u][2 * j + 1]));
+                  pk[j] = relu_pk16<PREC>(__uint_as_float(v[u][2 * j]), __uint_as_float(v[u][2 * j + 1]));
                 tmem_st16(acol + cc * 16, pk);
               } else {
                 uint32_t hv[32];

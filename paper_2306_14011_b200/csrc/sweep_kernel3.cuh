@@ -1,4 +1,4 @@
-// K1, BF16 variant with three 128-row tiles in flight per SM (nets with at
+// K1, 16-bit variant (BF16, or FP16 with PREC = PREC_FP16) with three 128-row tiles in flight per SM (nets with at
 // most one hidden->hidden layer: 14-H-1 and 14-H-H-1, H <= 128).
 //
 // TMEM per slot is just the H-column accumulator region D:
@@ -142,7 +142,7 @@ __device__ __forceinline__ float final_compute(const KParams& p, const uint32_t 
   return ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
 }
 
-template <int H, int SPG, int NS>
+template <int H, int SPG, int NS, int PREC = PREC_BF16>
 __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     sweep_kernel3(const __grid_constant__ KParams p, int mode) {
   // SPG = parameter slots per decoder group: 4 (two A0 columns per 8-byte table
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     uint32_t ones[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) ones[j] = 0u;
-    ones[0] = 0x00003F80u;  // bf16 1.0 in K slot 0
+    ones[0] = one16<PREC>();  // 1.0 in K slot 0
     if (C::A0_SMEM) {
       st_a0_smem(smem + p.smem_ones, warp * 32u + lane, ones);
       fence_proxy_async_smem();
@@ -263,9 +263,9 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     if (x_full(tl_)) {
       mbar_wait(xbar, phx);
       phx ^= 1u;
-      make_a0_row<PREC_BF16, true>(p, reinterpret_cast<const float*>(xs) + row * p.P, a);
+      make_a0_row<PREC, true>(p, reinterpret_cast<const float*>(xs) + row * p.P, a);
     } else {
-      make_a0_predict<PREC_BF16>(p, I_ < p.end ? I_ : p.begin, a);
+      make_a0_predict<PREC>(p, I_ < p.end ? I_ : p.begin, a);
     }
   };
 
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
   if (tile < p.num_tiles) {
     if (PRED) a0_pred(tile, I, a0);
     else if (SPG == 4) make_a0_sweep4(p, slut, D, a0);
-    else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
+    else make_a0_sweep<PREC>(p, slut, D, a0);
     put_a0(a0);
     if (!C::A0_SMEM) tmem_wait_st();
     issue(0);  // L1 of the first tile
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
         }
         else {
           odometer_step_n<NG>(p.R, p.dD, D);
-          if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
+          if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC>(p, slut, D, a0);
         }
         put_a0(a0);
         if (!C::A0_SMEM) tmem_wait_st();
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            pk[j] = relu_bf16x2(__uint_as_float(v[u][2 * j]), __uint_as_float(v[u][2 * j + 1]));
+            pk[j] = relu_pk16<PREC>(__uint_as_float(v[u][2 * j]), __uint_as_float(v[u][2 * j + 1]));
           tmem_st16(dcol + (c + u) * 16, pk);
         }
       }
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
         }
         else {
           odometer_step_n<NG>(p.R, p.dD, D);
-          if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC_BF16>(p, slut, D, a0);
+          if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC>(p, slut, D, a0);
         }
         put_a0(a0);
       }

@@ -12,17 +12,27 @@
 // BF16 kernel there is no central MMA warp: after the slot's warps pass a
 // named barrier, one elected lane of the slot's first warp issues the layer's
 // fully unrolled UMMA chain (kind::tf32, A from TMEM) and commits it.
+//
+// PREC_FP32H: the FP32 path as 3xFP16 (kind::f16 at twice the kind::tf32 rate;
+// fp16 hi + fp16 lo carry 22 significant bits, the same as the tf32 split).
+// The hidden epilogue packs A = [hi | lo] IN PLACE over the D1 columns it reads
+// (32-column chunk c -> 16 hi columns at 32c, 16 lo columns at 32c + 16), the
+// last layer accumulates into its own region Y, and the layer-1 operand A0
+// (hi and lo tiles) lives in shared memory (SS-form UMMA), so a slot needs
+// only 2H columns: two slots at H = 128.
 #pragma once
 #include "sweep_kernel.cuh"
+#include "sweep_kernel3.cuh"  // st_a0_smem
 
 namespace surr {
 
 template <int PREC, int H>
 struct Cfg5 {
-  static constexpr int A_COLS = PREC == PREC_FP32 ? 2 * H : H;
+  static constexpr bool H16 = PREC == PREC_FP32H;  // 3xFP16, A packed in place, A0 in smem
+  static constexpr int A_COLS = H16 ? 0 : PREC == PREC_FP32 ? 2 * H : H;
   // FP32: the last layer accumulates into its own region Y = D2, so the next
   // tile's layer-1 UMMA (into D1) overlaps this tile's final layer (reads D2)
-  static constexpr bool SEP_Y = PREC == PREC_FP32;
+  static constexpr bool SEP_Y = PREC == PREC_FP32 || H16;
   static constexpr int SLOT_COLS = H + A_COLS + (SEP_Y ? H : 0);
   static constexpr int Y_COL = H + A_COLS;  // D2 region (SEP_Y)
   static constexpr int NSLOT = 512 / SLOT_COLS >= 2 ? 2 : 1;
@@ -32,7 +42,7 @@ struct Cfg5 {
   static constexpr int NEED = NSLOT * SLOT_COLS;
   static constexpr int TMEM_COLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
   static constexpr int THREADS = 128 * NSLOT * NSUB;
-  static constexpr int THREE_H = PREC == PREC_FP32;  // 3 passes in hidden layers
+  static constexpr int THREE_H = PREC == PREC_FP32 || H16;  // 3 passes in hidden layers
   static constexpr int A0_LO = PREC == PREC_FP32 ? H : K0;
   static_assert(NEED <= 512, "TMEM budget");
 };
@@ -47,7 +57,8 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_misc);  // [0] load, [4 + s] d ready
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.smem_misc + 64);
-  float* red = reinterpret_cast<float*>(smem + p.smem_a0);           // [slot][sub][row] partials
+  // [slot][sub][row] partials (3xFP16: after the shared-memory A0 tiles)
+  float* red = reinterpret_cast<float*>(smem + (C::H16 ? p.smem_ones + 4096 : p.smem_a0));
   TopkShared ts;
   ts.lists = reinterpret_cast<surr_record*>(smem + p.smem_lists);
   ts.cand = reinterpret_cast<surr_record*>(smem + p.smem_cand);
@@ -93,7 +104,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
   const uint32_t tl = (wq * 32u) << 16;
   const uint32_t dslot = tmem_base + s * C::SLOT_COLS;  // lane-0 view (UMMA operands)
   const uint32_t dcol = dslot + tl + q * C::CPS;         // this warp's D columns
-  const uint32_t acol = dslot + tl + H;                  // this warp's A region
+  const uint32_t acol = dslot + tl + (C::H16 ? 0 : H);   // this warp's A region
   const uint8_t* slut = smem + p.smem_lut;
   surr_record* mycand = ts.cand + (size_t)(s * 4 + wq) * CAND_CAP;
   uint32_t ncand = 0;
@@ -105,6 +116,10 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
   const uint64_t d_b2 = make_bdesc(sb + p.off_bh, p.sbo_bh);
   const uint64_t d_b2lo = make_bdesc(sb + p.off_bh + p.lo_delta_h, p.sbo_bh);
   const uint32_t idesc = p.idesc;
+  uint8_t* a0h_tile = smem + p.smem_a0 + s * 2 * 4096;  // 3xFP16: A0 hi / lo tiles of this slot
+  uint8_t* a0l_tile = a0h_tile + 4096;
+  const uint64_t d_a0h = make_bdesc(sb + p.smem_a0 + s * 2 * 4096, 256);
+  const uint64_t d_a0l = make_bdesc(sb + p.smem_a0 + s * 2 * 4096 + 4096, 256);
 
   auto issue = [&](int layer) {
     tc_fence_before();
@@ -113,7 +128,20 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
       tc_fence_after();
       if (elect_one()) {
         const uint32_t a = dslot + H;
-        if (layer == 0) {
+        if (C::H16 && layer == 0) {
+          umma_f16_ss(dslot, d_a0h, d_b1, idesc, 0u);
+          umma_f16_ss(dslot, d_a0l, d_b1, idesc, 1u);
+          umma_f16_ss(dslot, d_a0h, d_b1lo, idesc, 1u);
+        } else if (C::H16) {
+          const uint32_t d2 = dslot + C::Y_COL;
+#pragma unroll
+          for (int kk = 0; kk < H / 16; ++kk) {
+            const uint32_t ah = dslot + 32 * (kk >> 1) + 8 * (kk & 1);  // hi; lo at + 16
+            umma_f16_ts(d2, ah, d_b2 + kk * 16, idesc, kk > 0);
+            umma_f16_ts(d2, ah + 16, d_b2 + kk * 16, idesc, 1u);
+            umma_f16_ts(d2, ah, d_b2lo + kk * 16, idesc, 1u);
+          }
+        } else if (layer == 0) {
 #pragma unroll
           for (int kk = 0; kk < K0 / 8; ++kk) {
             umma_tf32_ts(dslot, a + kk * 8, d_b1 + kk * 16, idesc, kk > 0);
@@ -146,10 +174,16 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
   mbar_wait(&bars[0], 0);
 
   A0Regs a0;
-  auto put_a0 = [&]() {  // sub 0 stores the layer-1 operand (tf32 hi / lo slots)
-    tmem_st16(acol, a0.hi);
-    tmem_st16(acol + C::A0_LO, a0.lo);
-    tmem_wait_st();
+  auto put_a0 = [&]() {  // sub 0 stores the layer-1 operand (tf32 hi / lo slots, or fp16 tiles)
+    if (C::H16) {
+      st_a0_smem(a0h_tile, row, a0.hi);
+      st_a0_smem(a0l_tile, row, a0.lo);
+      fence_proxy_async_smem();
+    } else {
+      tmem_st16(acol, a0.hi);
+      tmem_st16(acol + C::A0_LO, a0.lo);
+      tmem_wait_st();
+    }
   };
   if (first && tile < p.num_tiles) {
     if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, I < p.end ? I : p.begin, a0);
@@ -174,7 +208,25 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
       if (l + 1 < p.NL) {
         // a5: hidden epilogue over this sub's columns -> A (tf32 hi [, lo])
 #pragma unroll
-        for (int c = 0; c < C::CPS / 32; ++c) {
+        for (int c = 0; C::H16 && c < C::CPS / 32; ++c) {
+          // in place: chunk c (32 fp32 columns, read first) -> 16 hi + 16 lo fp16x2 columns
+          uint32_t v[32];
+          tmem_ld32(dcol + c * 32, v);
+          tmem_wait_ld();
+          uint32_t hv[16], lv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float x0 = fmaxf(__uint_as_float(v[2 * j]), 0.0f), x1 = fmaxf(__uint_as_float(v[2 * j + 1]), 0.0f);
+            hv[j] = f16x2(x0, x1);
+            float h0, h1;
+            f16x2_to_f32(hv[j], h0, h1);
+            lv[j] = f16x2(x0 - h0, x1 - h1);  // x - hi is exact in fp32; one rounding to fp16
+          }
+          tmem_st16(dcol + c * 32, hv);
+          tmem_st16(dcol + c * 32 + 16, lv);
+        }
+#pragma unroll
+        for (int c = 0; !C::H16 && c < C::CPS / 32; ++c) {
           uint32_t v[32];
           tmem_ld32(dcol + c * 32, v);
           tmem_wait_ld();

@@ -47,7 +47,7 @@ struct CfgPair {
 
 enum { PB_LOAD = 0, PB_A0F = 1, PB_AQ = 2, PB_RF = 6, PB_DA = 7, PB_DB = 8, PB_A0E = 9 };
 
-template <int H, int SPG, int NS>
+template <int H, int SPG, int NS, int PREC = PREC_BF16>
 __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
     sweep_kernel_pair(const __grid_constant__ KParams p, int mode) {
   using C = CfgPair<H, NS>;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
     uint32_t ones[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) ones[j] = 0u;
-    ones[0] = 0x00003F80u;
+    ones[0] = one16<PREC>();
     st_a0_smem(smem + p.smem_ones, (warp - 4) * 32u + lane, ones);
     fence_proxy_async_smem();
   }
@@ -230,10 +230,10 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
         A0Regs a0;
         const uint64_t I = I0 + 32u * u;
         if (mode == MODE_PREDICT) {
-          make_a0_predict<PREC_BF16>(p, I < p.end ? I : p.begin, a0);
+          make_a0_predict<PREC>(p, I < p.end ? I : p.begin, a0);
         } else {
           if (tile != pair) odometer_step_n<NG>(p.R, p.dD, D[u]);
-          if (SPG == 4) make_a0_sweep4(p, slut, D[u], a0); else make_a0_sweep<PREC_BF16>(p, slut, D[u], a0);
+          if (SPG == 4) make_a0_sweep4(p, slut, D[u], a0); else make_a0_sweep<PREC>(p, slut, D[u], a0);
         }
         st_a0_smem(a0tile, lane + 32u * u, a0.hi);
       }
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
               uint32_t pk[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i)
-                pk[i] = relu_bf16x2(__uint_as_float(v[c][2 * i]), __uint_as_float(v[c][2 * i + 1]));
+                pk[i] = relu_pk16<PREC>(__uint_as_float(v[c][2 * i]), __uint_as_float(v[c][2 * i + 1]));
               tmem_st16(dcol + (j * C::QC + c * 32) / 2, pk);
             }
             tmem_wait_st();

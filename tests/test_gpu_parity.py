@@ -42,7 +42,7 @@ def test_decode_bit_exact(pk, name, first, n):
 
 
 # ------------------------------------------------------------------ dense t(I)
-@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "fp32_3xtf32", "tf32", "fp16", "bf16"])
 def test_tiny_all_times(pk, prec):
     vl = workloads.space("tiny")
     model = workloads.load_model("tiny_14-32-32-1")
@@ -53,7 +53,7 @@ def test_tiny_all_times(pk, prec):
     assert e.max() <= TOL[prec], f"{prec}: max rel err {e.max():.3e}"
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "fp32_3xtf32", "tf32", "fp16", "bf16"])
 @pytest.mark.parametrize("begin,n", [(0, 1 << 18), (98_765_431, (1 << 18) + 77), (170859375 - 100003, 100003)])
 def test_cfg2_slice_times(pk, prec, begin, n):
     vl = workloads.space("cfg2")
@@ -68,16 +68,16 @@ def test_cfg2_slice_times(pk, prec, begin, n):
 def test_predict_matches_oracle_and_sweep_bitwise(pk):
     vl = workloads.space("cfg2")
     model = workloads.load_model("cfg2_14-128-128-1")
-    for prec in ["bf16", "fp32"]:
+    for prec in ["bf16", "fp16", "fp32", "fp32_3xtf32"]:
         h = _handle(pk, model, prec)
         # rows = configs [b, b+n) so predict and the dense sweep see identical inputs
         b, n = 5_000_017, 3001
         X = ospace.values_of(ospace.decode(np.arange(b, b + n, dtype=np.uint64), workloads.radices("cfg2")), vl)
         tp = h.predict(torch.tensor(X, dtype=torch.float32, device="cuda:0")).cpu().numpy()
         ts = h.eval_range(vl, b, b + n).cpu().numpy()
-        assert np.array_equal(tp, ts)
+        assert np.array_equal(tp, ts), f"{prec}: {np.count_nonzero(tp != ts)} rows differ"
         e = rel_err(tp, osweep.times(model, vl, b, b + n), model["y_scale"])
-        assert e.max() <= TOL[prec]
+        assert e.max() <= TOL[prec], f"{prec}: max rel err {e.max():.3e}"
         assert h.predict(torch.zeros((0, 14), dtype=torch.float32, device="cuda:0")).numel() == 0
 
 
@@ -92,7 +92,8 @@ def test_tiny_top1_exact_fp32(pk):
     assert rel_err(t.cpu().numpy(), rt, model["y_scale"]).max() <= TOL["fp32"]
 
 
-@pytest.mark.parametrize("prec,k", [("fp32", 16), ("bf16", 16), ("tf32", 64), ("bf16", 1024), ("fp32", 1000)])
+@pytest.mark.parametrize("prec,k", [("fp32", 16), ("bf16", 16), ("tf32", 64), ("bf16", 1024), ("fp32", 1000),
+                                    ("fp16", 16), ("fp16", 1024), ("fp32_3xtf32", 64)])
 def test_cfg2_subrange_topk(pk, prec, k):
     vl = workloads.space("cfg2")
     model = workloads.load_model("cfg2_14-128-128-1")
@@ -105,7 +106,7 @@ def test_cfg2_subrange_topk(pk, prec, k):
                lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
 
 
-@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("prec", ["bf16", "fp16", "fp32", "fp32_3xtf32"])
 def test_cfg2_full_sweep_reevaluated(pk, prec):
     vl = workloads.space("cfg2")
     model = workloads.load_model("cfg2_14-128-128-1")
@@ -127,7 +128,7 @@ def test_all_ties_net_full_size(pk):
     assert idx.cpu().numpy().tolist() == list(range(b, b + 64))
 
 
-@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "bf16", "fp16"])
 def test_affine_net_closed_form_full_cfg5(pk, prec):
     vl = workloads.space("cfg5")
     model = workloads.affine_net(vl, [128, 128], seed=11)
@@ -216,46 +217,49 @@ def test_ensemble_fp32_path_and_chunking(pk):
 
 
 # ------------------------------------------------------------------ CTA pairs (cfg3, H = 256)
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
 @pytest.mark.parametrize("hidden", [[256], [256, 256], [256, 256, 256]])
-def test_pair_kernel_random_nets(pk, hidden):
+def test_pair_kernel_random_nets(pk, hidden, prec):
     # cta_group::2 kernel over ragged ranges (odd pair-tile counts, tails inside rank 1)
     vl = workloads.space("cfg3")
     model = workloads.random_net(vl, hidden, seed=len(hidden) + 40)
-    h = _handle(pk, model, "bf16")
+    h = _handle(pk, model, prec)
     for b, n in [(0, 256 * 148 * 2 + 129), (1_279_000_000 - 70_001, 70_001), (5, 3)]:
         t = h.eval_range(vl, b, b + n).cpu().numpy()
         ref = osweep.times(model, vl, b, b + n)
         e = rel_err(t, ref, model["y_scale"])
-        assert e.max() <= TOL["bf16"], f"{hidden} [{b},{b + n}): max rel err {e.max():.3e}"
+        assert e.max() <= TOL[prec], f"{hidden} [{b},{b + n}): max rel err {e.max():.3e}"
 
 
-def test_cfg3_trained_slice_and_topk(pk):
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
+def test_cfg3_trained_slice_and_topk(pk, prec):
     vl = workloads.space("cfg3")
     model = workloads.load_model("cfg3_14-256-256-256-1")
-    h = _handle(pk, model, "bf16")
+    h = _handle(pk, model, prec)
     b, n = 640_000_017, (1 << 18) + 333
     t = h.eval_range(vl, b, b + n).cpu().numpy()
     ref = osweep.times(model, vl, b, b + n)
-    assert rel_err(t, ref, model["y_scale"]).max() <= TOL["bf16"]
+    assert rel_err(t, ref, model["y_scale"]).max() <= TOL[prec]
     idx, tk, cnt = h.sweep(vl, 64, b, b + n)
     ri, rt = osweep.topk(model, vl, 64, b, b + n)
     assert cnt == 64
     check_topk(idx.cpu().numpy().astype(np.uint64), tk.cpu().numpy(), ri, rt,
-               lambda i: osweep.times_at(model, vl, i), TOL["bf16"], model["y_scale"])
+               lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
     X = ospace.values_of(ospace.decode(np.arange(b, b + 3000, dtype=np.uint64), workloads.radices("cfg3")), vl)
     tp = h.predict(torch.tensor(X, dtype=torch.float32, device="cuda:0")).cpu().numpy()
     assert np.array_equal(tp, t[:3000])
 
 
-def test_cfg3_full_sweep_reevaluated(pk):
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
+def test_cfg3_full_sweep_reevaluated(pk, prec):
     vl = workloads.space("cfg3")
     model = workloads.load_model("cfg3_14-256-256-256-1")
-    h = _handle(pk, model, "bf16")
+    h = _handle(pk, model, prec)
     idx, t, cnt = h.sweep(vl, 64)
     idx = idx.cpu().numpy().astype(np.uint64)
     t = t.cpu().numpy()
     assert cnt == 64 and np.all(np.diff(t) >= 0)
-    assert rel_err(t, osweep.times_at(model, vl, idx), model["y_scale"]).max() <= TOL["bf16"]
+    assert rel_err(t, osweep.times_at(model, vl, idx), model["y_scale"]).max() <= TOL[prec]
 
 
 # ------------------------------------------------------------------ the paper's space
