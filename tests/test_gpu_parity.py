@@ -321,3 +321,60 @@ def test_predict_staged_rows_large_batch(pk):
     sample = np.random.default_rng(3).integers(0, n, 4000)
     ref = osweep.times_at(model, vl, (b + sample).astype(np.uint64))
     assert rel_err(tp[sample], ref, model["y_scale"]).max() <= TOL["bf16"]
+
+
+# ------------------------------------------------------------------ precisions (FP16, 3xFP16 FP32 path)
+@pytest.mark.parametrize("prec", ["fp16", "fp32", "bf16"])
+def test_cfg5_trained_slices_and_topk1024(pk, prec):
+    # the cfg5 net (the headline space of the 8-GPU sweep) on ragged windows at
+    # both ends of the u64 index range, plus a k = 1024 sub-range top-k
+    vl = workloads.space("cfg5")
+    model = workloads.load_model("cfg5_14-128-128-1")
+    h = _handle(pk, model, prec)
+    for b, n in [(0, (1 << 18) + 5), (13_492_928_512 - 200_003, 200_003), (6_746_464_256, 1 << 18)]:
+        t = h.eval_range(vl, b, b + n).cpu().numpy()
+        e = rel_err(t, osweep.times(model, vl, b, b + n), model["y_scale"])
+        assert e.max() <= TOL[prec], f"{prec} [{b}, {b + n}): max rel err {e.max():.3e}"
+    b, e_ = 9_876_543_210, 9_876_543_210 + (1 << 20) + 99
+    idx, tk, cnt = h.sweep(vl, 1024, b, e_)
+    ri, rt = osweep.topk(model, vl, 1024, b, e_)
+    assert cnt == 1024
+    check_topk(idx.cpu().numpy().astype(np.uint64), tk.cpu().numpy(), ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
+
+
+def test_fp32_path_kernel_choice(pk):
+    # <= 2 hidden layers, H <= 128: 3xFP16 on kind::f16; deeper nets: 3xTF32
+    # (general kernel; its weights fit one SM up to H = 64 at 3 hidden layers)
+    vl = workloads.space("cfg2")
+    h = _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp32")
+    assert h.arith()[:2] == ("f16", 3)
+    assert _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp32_3xtf32").arith()[:2] == ("tf32", 3)
+    assert _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp16").arith()[:2] == ("f16", 1)
+    deep = workloads.random_net(vl, [64, 64, 64], seed=5)
+    h = _handle(pk, deep, "fp32")
+    assert h.arith()[:2] == ("tf32", 3)
+    b, n = 100_000_003, 70_001
+    t = h.eval_range(vl, b, b + n).cpu().numpy()
+    assert rel_err(t, osweep.times(deep, vl, b, b + n), deep["y_scale"]).max() <= TOL["fp32"]
+    # issued tensor work of the cfg2 net: 16-bit L1 + (H + 16) x H bias-folded L2
+    assert _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp16").arith()[2] == 2 * (16 * 128 + 144 * 128)
+
+
+@pytest.mark.parametrize("prec", ["fp16", "fp32"])
+def test_fp16_range_guard(pk, prec):
+    # activations that can exceed 65504 over the space are refused (SURR_E_RANGE),
+    # the same net runs on BF16 / 3xTF32
+    vl = workloads.space("cfg2")
+    model = workloads.random_net(vl, [128, 128], seed=9)
+    big = dict(model)
+    big["members"] = [dict(m) for m in model["members"]]
+    m0 = big["members"][0]
+    m0["W"] = [w.copy() for w in m0["W"]]
+    m0["W"][0] = m0["W"][0] * 1e4   # |W1| <= 4e3 loads; h1 can reach ~1e5 over the space
+    h = _handle(pk, big, prec)
+    with pytest.raises(pk.SurrogateError, match="FP16"):
+        h.sweep(vl, 4, 0, 1000)
+    safe = "bf16" if prec == "fp16" else "fp32_3xtf32"
+    t = _handle(pk, big, safe).eval_range(vl, 0, 1000).cpu().numpy()
+    assert rel_err(t, osweep.times(big, vl, 0, 1000), big["y_scale"]).max() <= TOL[safe] * 10
