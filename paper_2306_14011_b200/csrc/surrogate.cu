@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -645,6 +646,7 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
       L.p.x_tma = (L.ki.x_stage && x && ((uintptr_t)x % 16) == 0 && (c0 * L.p.P * 4) % 16 == 0) ? 1u : 0u;
       L.p.trace = h->trace;
       L.p.trace_n = h->trace_n;
+      { const char* v = getenv("SURR_VARIANT"); L.p.variant = v ? (uint32_t)atoi(v) : 0u; }
       rc = launch(h, L, m, st);
       if (rc) return rc;
     }

@@ -103,6 +103,7 @@ struct KParams {
   // debug timeline (CTA 0 only): trace[ev] = clock64 of event ev, or null
   unsigned long long* trace;
   uint32_t trace_n;
+  uint32_t variant;  // schedule variant (development A/B switch, env SURR_VARIANT; 0 = default)
 };
 
 static_assert(offsetof(KParams, fin_w) % 16 == 0 && offsetof(KParams, fin_nb) % 16 == 0,

@@ -185,6 +185,9 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
       tmem_wait_st();
     }
   };
+  // separate Y region only with a hidden->hidden layer (14-H-1 nets: the final
+  // layer reads D1, and the next L1 waits for those reads at the slot barrier)
+  const bool sep = C::SEP_Y && p.NL > 1;
   if (first && tile < p.num_tiles) {
     if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, I < p.end ? I : p.begin, a0);
     else make_a0_sweep<PREC>(p, slut, D, a0);
@@ -243,13 +246,13 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
         tmem_wait_st();
         if (tr) trace_ev(p, s, jr, 2);
         issue(1);
-        if (C::SEP_Y && first && has_next) {  // next tile's digits / row while L2 runs
+        if (sep && first && has_next) {  // next tile's digits / row while L2 runs
           if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
           else odometer_step(p.R, p.dD, D);
         }
       } else {
         // a7: final-layer partial over this sub's columns (relu(x + b) = max(x, -b) + b)
-        if (C::SEP_Y && has_next) {
+        if (sep && has_next) {
           // D2 ready => L2 no longer reads A: store the next A0 there and start
           // the next tile's layer 1 (into D1) before reading D2
           if (first) {
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
           }
           issue(0);
         }
-        const uint32_t fcol = dcol + (C::SEP_Y ? C::Y_COL : 0);
+        const uint32_t fcol = dcol + (sep ? C::Y_COL : 0);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
         for (int c = 0; c < C::CPS / 32; ++c) {
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
       }
     }
     // next tile's A0 (sub 0) and the next layer-1 UMMA as soon as D is free
-    if (!C::SEP_Y && first && has_next) {
+    if (!sep && first && has_next) {
       if (mode == MODE_PREDICT) {
         make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
       } else {
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
     }
     if (tr) trace_ev(p, s, jr, 5);
     if (C::NSUB > 1 && !last) red[(s * C::NSUB + q) * TILE_M + row] = part;
-    if (!C::SEP_Y && has_next) issue(0);  // includes the slot barrier: partials are visible after it
+    if (!sep && has_next) issue(0);  // includes the slot barrier: partials are visible after it
     else named_bar_sync(bar_id, 128 * C::NSUB);
     if (tr) trace_ev(p, s, jr, 6);
     if (last) {

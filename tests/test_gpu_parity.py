@@ -371,10 +371,28 @@ def test_fp16_range_guard(pk, prec):
     big["members"] = [dict(m) for m in model["members"]]
     m0 = big["members"][0]
     m0["W"] = [w.copy() for w in m0["W"]]
-    m0["W"][0] = m0["W"][0] * 1e4   # |W1| <= 4e3 loads; h1 can reach ~1e5 over the space
+    m0["W"][0] = m0["W"][0] * 1e5   # |W1| <= 2e4 loads; the bound on h1 exceeds 65504
     h = _handle(pk, big, prec)
     with pytest.raises(pk.SurrogateError, match="FP16"):
         h.sweep(vl, 4, 0, 1000)
     safe = "bf16" if prec == "fp16" else "fp32_3xtf32"
     t = _handle(pk, big, safe).eval_range(vl, 0, 1000).cpu().numpy()
     assert rel_err(t, osweep.times(big, vl, 0, 1000), big["y_scale"]).max() <= TOL[safe] * 10
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp32_3xtf32", "tf32", "fp16", "bf16"])
+@pytest.mark.parametrize("hidden", [[32], [64], [128], [32, 32], [64, 64]])
+def test_shallow_and_narrow_nets(pk, prec, hidden):
+    # one hidden layer (14-H-1: the final layer reads the layer-1 accumulator) and
+    # narrow two-layer nets (N-halves of 16 / 32 columns) on ragged ranges
+    vl = workloads.space("cfg2")
+    model = workloads.random_net(vl, hidden, seed=sum(hidden) + len(hidden))
+    h = _handle(pk, model, prec)
+    for b, n in [(0, 148 * 2 * 128 + 77), (170859375 - 40_001, 40_001)]:
+        t = h.eval_range(vl, b, b + n).cpu().numpy()
+        e = rel_err(t, osweep.times(model, vl, b, b + n), model["y_scale"])
+        assert e.max() <= TOL[prec], f"{prec} {hidden} [{b}, {b + n}): max rel err {e.max():.3e}"
+    idx, tk, cnt = h.sweep(vl, 32, 1_000_003, 1_000_003 + 300_000)
+    ri, rt = osweep.topk(model, vl, 32, 1_000_003, 1_000_003 + 300_000)
+    check_topk(idx.cpu().numpy().astype(np.uint64), tk.cpu().numpy(), ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
