@@ -181,6 +181,7 @@ struct KernelInfo {
   bool pair = false;       // CTA-pair kernel (cluster of 2, cta_group::2, 256-row tiles)
   bool x_stage = false;    // predict rows staged in shared memory by bulk copies
   uint32_t a0_tiles = 1;   // shared-memory A0 tiles per slot (3xFP16: hi + lo)
+  bool acc_stage = false;  // ensemble accumulator prefetched per tile into shared memory by bulk copies
 };
 
 template <int H, int SPG, int PREC>
@@ -219,6 +220,7 @@ KernelInfo kinfo3() {
   KernelInfo ki{(const void*)&sweep_kernel3<H, SPG, NS, PREC>, C::NSLOT, C::THREADS, true};
   ki.a0_smem = C::A0_SMEM;
   ki.x_stage = SPG == 0;  // the predict instantiation
+  ki.acc_stage = true;
   return ki;
 }
 
@@ -304,7 +306,9 @@ size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_
   off += (mode == MODE_TOPK ? (size_t)nslot * 4 * CAND_CAP * sizeof(surr_record) : 0);  // last-sub warps
   off = align_up(off, 128);
   p.smem_misc = (uint32_t)off;
-  off += 256;
+  off += 512;  // mbarriers [0 .. 31], TMEM slot address (+64), top-k scalars (+128), staging barriers (+256)
+  p.smem_acc = (uint32_t)align_up(off, 128);
+  off = p.smem_acc + (ki.acc_stage ? (size_t)nslot * 2 * TILE_M * 4 : 0);
   off = align_up(off, 1024);
   p.smem_a0 = (uint32_t)off;
   off += ki.a0_smem ? (size_t)nslot * ki.a0_tiles * 4096 : ki.red_bytes;
@@ -638,6 +642,8 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
         L.p.t_acc = h->d_acc;
         L.p.acc_base = c0;
         L.p.inv_e = 1.0f / (float)E;
+        // members >= 1 read t_acc[I - c0]: tile-aligned, so 512-byte bulk copies per tile
+        L.p.acc_tma = (L.ki.acc_stage && e > 0 && ((uintptr_t)h->d_acc % 16) == 0) ? 1u : 0u;
       }
       L.p.recs = h->d_recs + done * k;
       L.p.t_dense = t_dense ? t_dense + (c0 - begin) : nullptr;
@@ -647,6 +653,7 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
       L.p.trace = h->trace;
       L.p.trace_n = h->trace_n;
       { const char* v = getenv("SURR_VARIANT"); L.p.variant = v ? (uint32_t)atoi(v) : 0u; }
+      if (L.p.variant == 4) L.p.acc_tma = 0;  // A/B: accumulator read at use
       rc = launch(h, L, m, st);
       if (rc) return rc;
     }

@@ -100,6 +100,7 @@ struct KParams {
   uint64_t acc_base;
   uint32_t acc_mode;
   float inv_e;
+  uint32_t smem_acc, acc_tma;  // 4-slot kernel: per-slot double buffer of a tile's t_acc (bulk copies)
   // debug timeline (CTA 0 only): trace[ev] = clock64 of event ev, or null
   unsigned long long* trace;
   uint32_t trace_n;

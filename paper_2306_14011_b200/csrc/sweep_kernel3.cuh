@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       for (int s = 0; s < C::NSLOT; ++s) mbar_init(&bars[4 + s], 1);
       if (PRED)
         for (int s = 0; s < C::NSLOT; ++s) mbar_init(&bars[9 + s], 1);  // row staging (tmem_slot is at +64)
+      for (int s = 0; s < 2 * C::NSLOT; ++s) mbar_init(&bars[32 + s], 1);  // ensemble accumulator staging
       fence_mbar_init();
       fence_proxy_async_smem();
       const uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
@@ -269,6 +270,31 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     }
   };
 
+  // ensemble members >= 1: the slot's tile of the fp32 accumulator is bulk-copied
+  // into a per-slot double buffer when the tile's L1 is issued, and read when
+  // the tile's prediction is final (~3k cycles later: the HBM latency is hidden)
+  uint8_t* accb = smem + p.smem_acc + s * 2 * TILE_M * 4;
+  uint32_t pha = 0;  // parity bits of the two buffers' barriers
+  auto acc_full = [&](uint64_t tl_) {
+    return p.acc_tma != 0u && p.acc_mode >= 2 && p.begin + (tl_ + 1) * TILE_M <= p.end;
+  };
+  auto acc_issue = [&](uint64_t tl_, uint32_t b) {  // one thread
+    if (tl_ < p.num_tiles && acc_full(tl_)) {
+      mbar_arrive_expect_tx(&bars[32 + 2 * s + b], TILE_M * 4);
+      bulk_g2s(accb + b * TILE_M * 4, p.t_acc + (p.begin + tl_ * TILE_M - p.acc_base), TILE_M * 4, &bars[32 + 2 * s + b]);
+    }
+  };
+  auto acc_get = [&](uint64_t tl_, uint32_t b, bool valid, uint64_t I_) -> float {
+    if (acc_full(tl_)) {
+      mbar_wait(&bars[32 + 2 * s + b], (pha >> b) & 1u);
+      pha ^= 1u << b;
+      return reinterpret_cast<const float*>(accb + b * TILE_M * 4)[row];
+    }
+    return ens_prefetch(p, valid, I_);
+  };
+  uint64_t acc_next = 0;  // tile whose accumulator the next phase-0 issue prefetches
+  uint32_t acc_buf = 0;   // ... and its buffer
+
   // every warp of the slot is done with its TMEM writes/reads -> issue one phase
   auto issue = [&](int phase) {
     tc_fence_before();
@@ -278,6 +304,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       if (elect_one()) {
         if (phase == 0) {
           if (PRED) x_issue(x_next);  // the A0 tile holds the rows now: the buffer is free
+          acc_issue(acc_next, acc_buf);
           if (C::A0_SMEM) umma_f16_ss(dslot, d_a0, d_b1, idesc_full, 0u);
           else umma_f16_ts(dslot, tmem_base + C::A0_COL + 8 * s, d_b1, idesc_full, 0u);
         } else {
@@ -305,6 +332,8 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
   if (PRED && issuer && elect_one()) x_issue(tile);
   __syncwarp();
   x_next = tile + p.dTiles;
+  acc_next = tile;
+  acc_buf = 0;
   if (tile < p.num_tiles) {
     if (PRED) a0_pred(tile, I, a0);
     else if (SPG == 4) make_a0_sweep4(p, slut, D, a0);
@@ -316,6 +345,8 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
   uint32_t jr = 0;
   for (; tile < p.num_tiles; tile += p.dTiles, ++jr) {
     const bool valid = I < p.end;
+    acc_next = tile + p.dTiles;  // the next phase-0 issue starts the next tile
+    acc_buf = (jr + 1) & 1u;
     const uint64_t In = I + dI;
     const bool has_next = tile + p.dTiles < p.num_tiles;
     const bool tr = wq == 0 && lane == 0;
@@ -402,9 +433,9 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       t = pa + pb;
     }
     t += p.c_out;
-    // (accumulator loaded here, not at the tile start: the 128-register budget
-    // of the 4-slot kernel has no room to carry it across the tile)
-    if (!ens_stage(p, valid, I, t, ens_prefetch(p, valid, I))) {
+    // (accumulator staged in shared memory since the tile's L1 issue: the
+    // 128-register budget of the 4-slot kernel has no room to carry it)
+    if (!ens_stage(p, valid, I, t, p.acc_mode >= 2 ? acc_get(tile, jr & 1u, valid, I) : 0.0f)) {
     } else if (mode == MODE_TOPK) {
       topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
     } else if (valid) {

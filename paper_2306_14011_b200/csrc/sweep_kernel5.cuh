@@ -69,6 +69,8 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
     if (lane == 0) {
       mbar_init(&bars[0], 1);
       for (int s = 0; s < C::NSLOT; ++s) mbar_init(&bars[4 + s], 1);
+      if (C::H16)  // 3xFP16: separate "L2 done" barriers (the next L1 is issued without a slot barrier)
+        for (int s = 0; s < C::NSLOT; ++s) mbar_init(&bars[6 + s], 1);
       fence_mbar_init();
       fence_proxy_async_smem();
       const uint32_t total = p.w_bytes + (mode == MODE_PREDICT ? 0u : p.lut_bytes);
@@ -121,12 +123,8 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
   const uint64_t d_a0h = make_bdesc(sb + p.smem_a0 + s * 2 * 4096, 256);
   const uint64_t d_a0l = make_bdesc(sb + p.smem_a0 + s * 2 * 4096 + 4096, 256);
 
-  auto issue = [&](int layer) {
-    tc_fence_before();
-    named_bar_sync(bar_id, 128 * C::NSUB);
-    if (issuer) {
-      tc_fence_after();
-      if (elect_one()) {
+  // one elected thread of the issuer warp: the layer's UMMA chain + commit
+  auto mma_chain = [&](int layer) {
         const uint32_t a = dslot + H;
         if (C::H16 && layer == 0) {
           umma_f16_ss(dslot, d_a0h, d_b1, idesc, 0u);
@@ -159,8 +157,14 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
             }
           }
         }
-        umma_commit(&bars[4 + s]);
-      }
+        umma_commit(&bars[(C::H16 && layer == 1) ? 6 + s : 4 + s]);
+  };
+  auto issue = [&](int layer) {
+    tc_fence_before();
+    named_bar_sync(bar_id, 128 * C::NSUB);
+    if (issuer) {
+      tc_fence_after();
+      if (elect_one()) mma_chain(layer);
       __syncwarp();
     }
   };
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
   const uint64_t dI = (uint64_t)p.dTiles * TILE_M;
   uint32_t D[MAXG];
   if (first && mode != MODE_PREDICT) init_digits(p.R, I, D);
-  uint32_t phd = 0;
+  uint32_t phd = 0, phd2 = 0;
   mbar_wait(&bars[0], 0);
 
   A0Regs a0;
@@ -204,8 +208,13 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
     const bool has_next = tile + p.dTiles < p.num_tiles;
     float part = 0.0f;
     for (uint32_t l = 0; l < p.NL; ++l) {
-      mbar_wait(&bars[4 + s], phd);
-      phd ^= 1u;
+      if (C::H16 && l == 1) {
+        mbar_wait(&bars[6 + s], phd2);
+        phd2 ^= 1u;
+      } else {
+        mbar_wait(&bars[4 + s], phd);
+        phd ^= 1u;
+      }
       tc_fence_after();
       if (tr) trace_ev(p, s, jr, 1 + 2 * l);
       if (l + 1 < p.NL) {
@@ -246,13 +255,33 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
         tmem_wait_st();
         if (tr) trace_ev(p, s, jr, 2);
         issue(1);
-        if (sep && first && has_next) {  // next tile's digits / row while L2 runs
+        if (C::H16 && sep && first && has_next) {
+          // 3xFP16: L1 of this tile is done, so the next tile's A0 tiles (shared
+          // memory) can be written now; sub 0's warps sync among themselves and
+          // the issuer starts the next L1 the moment L2 completes
+          if (mode == MODE_PREDICT) {
+            make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
+          } else {
+            odometer_step(p.R, p.dD, D);
+            make_a0_sweep<PREC>(p, slut, D, a0);
+          }
+          put_a0();
+          named_bar_sync(3 + s, 128);
+        } else if (sep && first && has_next) {  // next tile's digits / row while L2 runs
           if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, In < p.end ? In : p.begin, a0);
           else odometer_step(p.R, p.dD, D);
         }
       } else {
         // a7: final-layer partial over this sub's columns (relu(x + b) = max(x, -b) + b)
-        if (sep && has_next) {
+        if (C::H16 && sep && has_next) {
+          // L2 done (A free): the next tile's L1 into D1 while Y is read; its A0
+          // tiles were stored (and synced within sub 0) while L2 ran.  The L1 and
+          // L2 completions use separate mbarriers, so no slot barrier is needed
+          if (issuer) {
+            if (elect_one()) mma_chain(0);
+            __syncwarp();
+          }
+        } else if (sep && has_next) {
           // D2 ready => L2 no longer reads A: store the next A0 there and start
           // the next tile's layer 1 (into D1) before reading D2
           if (first) {

@@ -14,7 +14,7 @@ h.debug_trace(buf)
 h.sweep(vl, 16)
 torch.cuda.synchronize()
 t = buf.cpu().numpy().reshape(64, 4, 16).astype(np.float64)
-for s in range(2):
+for s in range(2):  # slot (trace rows of sub 0)
     d = t[10:40, s]
     if d[:, 0].min() <= 0: continue
     print("slot", s, "cycles per tile", np.median(np.diff(d[:, 0])))
