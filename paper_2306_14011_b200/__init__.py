@@ -55,9 +55,10 @@ def lib() -> ctypes.CDLL:
     """Load the in-tree CUDA library; raise loudly when it is absent."""
     global _LIB
     if _LIB is None:
-        if not os.path.exists(LIB_PATH):
-            raise SurrogateError(f"{LIB_PATH} not built (run __graft_entry__.build()); no CPU fallback exists")
-        L = ctypes.CDLL(LIB_PATH)
+        path = os.environ.get("SURR_LIB", LIB_PATH)  # development A/B of two in-tree builds
+        if not os.path.exists(path):
+            raise SurrogateError(f"{path} not built (run __graft_entry__.build()); no CPU fallback exists")
+        L = ctypes.CDLL(path)
         vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
         L.surrogate_create.argtypes = [i32, ctypes.POINTER(vp)]
         L.surrogate_destroy.argtypes = [vp]

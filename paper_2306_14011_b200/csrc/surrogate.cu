@@ -213,14 +213,14 @@ KernelInfo kinfo() {
   return KernelInfo{(const void*)&sweep_kernel<PREC, H>, C::NSLOT, C::THREADS, C::BIAS_MMA};
 }
 
-template <int H, int SPG, int PREC>
+template <int H, int SPG, int PREC, bool ENS = false>
 KernelInfo kinfo3() {
   constexpr int NS = 4;  // four 128-row tiles in flight per SM
   using C = Cfg3<H, NS>;
-  KernelInfo ki{(const void*)&sweep_kernel3<H, SPG, NS, PREC>, C::NSLOT, C::THREADS, true};
+  KernelInfo ki{(const void*)&sweep_kernel3<H, SPG, NS, PREC, ENS>, C::NSLOT, C::THREADS, true};
   ki.a0_smem = C::A0_SMEM;
   ki.x_stage = SPG == 0;  // the predict instantiation
-  ki.acc_stage = true;
+  ki.acc_stage = ENS;
   return ki;
 }
 
@@ -232,7 +232,7 @@ bool uses_quads(int prec, uint32_t H, uint32_t NL) {  // kernels with 4-paramete
 }
 
 template <int PREC>
-bool get_kernel16(uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg) {
+bool get_kernel16(uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg, bool ens) {
   // 16-bit nets whose weights exceed one SM (H = 256): CTA pairs
   if (H == 256) {
     *ki = spg == 4 ? kinfo_pair<256, 4, PREC>() : kinfo_pair<256, 2, PREC>();
@@ -250,6 +250,9 @@ bool get_kernel16(uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg) {
       return true;
     }
     if (H == 128) {
+      // ensembles (cfg 4): the accumulator-staging instantiations of the quad-table and predict kernels
+      if (ens && spg == 4) { *ki = kinfo3<128, 4, PREC, true>(); return true; }
+      if (ens && spg == 0) { *ki = kinfo3<128, 0, PREC, true>(); return true; }
       *ki = spg == 4 ? kinfo3<128, 4, PREC>() : spg == 2 ? kinfo3<128, 2, PREC>() : kinfo3<128, 0, PREC>();
       return true;
     }
@@ -257,9 +260,9 @@ bool get_kernel16(uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg) {
   return false;
 }
 
-bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg = 2) {
-  if (prec == PREC_BF16 && get_kernel16<PREC_BF16>(H, NL, ki, spg)) return true;
-  if (prec == PREC_FP16 && get_kernel16<PREC_FP16>(H, NL, ki, spg)) return true;
+bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg = 2, bool ens = false) {
+  if (prec == PREC_BF16 && get_kernel16<PREC_BF16>(H, NL, ki, spg, ens)) return true;
+  if (prec == PREC_FP16 && get_kernel16<PREC_FP16>(H, NL, ki, spg, ens)) return true;
   // FP32 (3xTF32) nets with at most one hidden->hidden layer: self-issuing, split
   // columns, separate D2 region (measured faster than the general kernel; for
   // 1xTF32 the general two-slot kernel measured faster, 572 vs 482 TFLOP/s)
@@ -366,7 +369,7 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
   if (uses_quads(h->prec, h->H, h->NL) && table_entries(4) * 8 <= 120 * 1024) {
     KernelInfo ki4;
     KParams tmp = h->mp;
-    if (get_kernel(h->prec, h->H, h->NL, &ki4, 4) &&
+    if (get_kernel(h->prec, h->H, h->NL, &ki4, 4, h->members.size() > 1) &&
         smem_layout(ki4, tmp, (uint32_t)align_up(table_entries(4) * 8, 16), std::max(k_hint, 1u), MODE_TOPK) <=
             SMEM_MAX)
       spg = 4;
@@ -502,7 +505,7 @@ struct Launch {
 };
 
 surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L, uint32_t member = 0) {
-  if (!get_kernel(h->prec, h->H, h->NL, &L->ki, mode == MODE_PREDICT ? 0 : h->spg))
+  if (!get_kernel(h->prec, h->H, h->NL, &L->ki, mode == MODE_PREDICT ? 0 : h->spg, h->members.size() > 1))
     return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
   KParams p = h->members.empty() ? h->mp : h->members[member];
   const KParams& s = h->sp;

@@ -142,7 +142,9 @@ __device__ __forceinline__ float final_compute(const KParams& p, const uint32_t 
   return ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
 }
 
-template <int H, int SPG, int NS, int PREC = PREC_BF16>
+// ENS: the ensemble-member instantiation (accumulator staging compiled in; the
+// single-net kernels carry none of it: it cost 4 % on cfg2 in a same-box A/B)
+template <int H, int SPG, int NS, int PREC = PREC_BF16, bool ENS = false>
 __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     sweep_kernel3(const __grid_constant__ KParams p, int mode) {
   // SPG = parameter slots per decoder group: 4 (two A0 columns per 8-byte table
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
   uint8_t* accb = smem + p.smem_acc + s * 2 * TILE_M * 4;
   uint32_t pha = 0;  // parity bits of the two buffers' barriers
   auto acc_full = [&](uint64_t tl_) {
-    return p.acc_tma != 0u && p.acc_mode >= 2 && p.begin + (tl_ + 1) * TILE_M <= p.end;
+    return ENS && p.acc_tma != 0u && p.acc_mode >= 2 && p.begin + (tl_ + 1) * TILE_M <= p.end;
   };
   auto acc_issue = [&](uint64_t tl_, uint32_t b) {  // one thread
     if (tl_ < p.num_tiles && acc_full(tl_)) {
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
       if (elect_one()) {
         if (phase == 0) {
           if (PRED) x_issue(x_next);  // the A0 tile holds the rows now: the buffer is free
-          acc_issue(acc_next, acc_buf);
+          if (ENS) acc_issue(acc_next, acc_buf);
           if (C::A0_SMEM) umma_f16_ss(dslot, d_a0, d_b1, idesc_full, 0u);
           else umma_f16_ts(dslot, tmem_base + C::A0_COL + 8 * s, d_b1, idesc_full, 0u);
         } else {
@@ -345,8 +347,10 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
   uint32_t jr = 0;
   for (; tile < p.num_tiles; tile += p.dTiles, ++jr) {
     const bool valid = I < p.end;
-    acc_next = tile + p.dTiles;  // the next phase-0 issue starts the next tile
-    acc_buf = (jr + 1) & 1u;
+    if (ENS) {
+      acc_next = tile + p.dTiles;  // the next phase-0 issue starts the next tile
+      acc_buf = (jr + 1) & 1u;
+    }
     const uint64_t In = I + dI;
     const bool has_next = tile + p.dTiles < p.num_tiles;
     const bool tr = wq == 0 && lane == 0;
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     t += p.c_out;
     // (accumulator staged in shared memory since the tile's L1 issue: the
     // 128-register budget of the 4-slot kernel has no room to carry it)
-    if (!ens_stage(p, valid, I, t, p.acc_mode >= 2 ? acc_get(tile, jr & 1u, valid, I) : 0.0f)) {
+    if (!ens_stage(p, valid, I, t, ENS ? acc_get(tile, jr & 1u, valid, I) : ens_prefetch(p, valid, I))) {
     } else if (mode == MODE_TOPK) {
       topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
     } else if (valid) {

@@ -29,6 +29,8 @@ METRICS = {
     "lts_bytes": "lts__t_bytes.sum",
     "tensor_pipe_active_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    # tensor memory (TMEM) activity: the epilogue / final-layer reads co-limit the 16-bit kernel
+    "tmem_active_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "fma_pipe_pct": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
     "registers_per_thread": "launch__registers_per_thread",
@@ -100,7 +102,7 @@ def main():
             d["tag"] = a.tag
             summary[key] = d
             md.append(f"## {key} — `{d['kernel'][:80]}` (ncu --set full, --clock-control none, one launch)")
-            for k2 in ["duration_ms", "sm_clock_ghz", "tensor_pipe_active_pct", "issue_active_pct", "alu_pipe_pct",
+            for k2 in ["duration_ms", "sm_clock_ghz", "tensor_pipe_active_pct", "tmem_active_pct", "issue_active_pct", "alu_pipe_pct",
                        "fma_pipe_pct", "dram_bytes_per_launch", "lts_bytes", "registers_per_thread", "grid_size",
                        "block_size", "smem_dynamic_bytes", "warp_instructions"]:
                 if k2 in d:
