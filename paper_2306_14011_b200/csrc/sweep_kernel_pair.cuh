@@ -301,7 +301,10 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
             tmem_ld32(dcol + c * 32, v[0]);
             tmem_ld32(dcol + (c + 1) * 32, v[1]);
             tmem_wait_ld();
-            if (c + 2 >= C::SUBC / 32) {  // region read: the next tile's layer 2 may overwrite it
+            // region read: the next tile's layer 2 may overwrite it (signalled only
+            // where the issuer waits for it: 14-H-1 nets, or subs != 2; an
+            // unwaited barrier phase is what compute-sanitizer's synccheck flags)
+            if (c + 2 >= C::SUBC / 32 && (p.NL == 1 || C::NSUB != 2)) {
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive_remote(&bars[PB_RF], 0);

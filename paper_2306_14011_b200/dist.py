@@ -13,8 +13,23 @@ One process per GPU (torchrun); ``torch.distributed`` is plumbing only.
 
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import torch
 import torch.distributed as dist
+
+
+@contextmanager
+def nvtx(name: str):
+    """NVTX range (sweep / allgather / merge) for nsys timelines; no-op without CUDA."""
+    on = torch.cuda.is_available()
+    if on:
+        torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        if on:
+            torch.cuda.nvtx.range_pop()
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -29,7 +44,8 @@ def gather_records(recs: torch.Tensor, group=None) -> torch.Tensor:
     """All ranks' [k, 2] int64 record blocks -> [W * k, 2] in rank order (one collective)."""
     world = dist.get_world_size(group)
     out = torch.empty((world * recs.shape[0], recs.shape[1]), dtype=recs.dtype, device=recs.device)
-    dist.all_gather_into_tensor(out, recs.contiguous(), group=group)
+    with nvtx("surrogate.allgather"):
+        dist.all_gather_into_tensor(out, recs.contiguous(), group=group)
     return out
 
 
@@ -39,8 +55,11 @@ def sweep_distributed(local_sweep, merge, n: int, k: int, group=None):
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     lo, hi = shard_range(n, world, rank)
-    recs = local_sweep(lo, hi, k)
-    return merge(gather_records(recs, group), world, k)
+    with nvtx("surrogate.sweep_shard"):
+        recs = local_sweep(lo, hi, k)
+    gathered = gather_records(recs, group)
+    with nvtx("surrogate.merge"):
+        return merge(gathered, world, k)
 
 
 def sweep(surrogate, value_lists, k: int, group=None):

@@ -1,0 +1,55 @@
+"""compute-sanitizer over small launches of every kernel family (SURVEY §5:
+race detection / sanitizers).  memcheck: out-of-bounds and misaligned global
+/ shared accesses; synccheck: illegal barrier use (named barriers, divergent
+__syncthreads); racecheck: shared-memory hazards between threads."""
+
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+from tests.helpers import need_gpu
+
+pytestmark = pytest.mark.gpu
+
+TARGET = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools", "sanitize_target.py")
+
+
+def _sanitizer():
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not found")
+    return exe
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_compute_sanitizer_clean(tool):
+    need_gpu()
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "97", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    res = subprocess.run(cmd + [sys.executable, TARGET], capture_output=True, text=True, timeout=1800)
+    out = res.stdout + res.stderr
+    assert "sanitize_target done" in out, out[-4000:]
+    assert res.returncode == 0 and "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+
+
+# the CTA top-k list is merged by one warp at a time under a shared-memory
+# spin lock (atomicCAS acquire / atomicExch release with block fences): the
+# lock hand-off orders the warps' list accesses, but racecheck models only
+# barrier synchronisation and reports those accesses as hazards.  Every other
+# shared-memory access must be hazard-free.
+LOCKED = {"warp_merge", "upper_bound_recs_fwd", "lower_bound_recs"}
+
+
+def test_compute_sanitizer_racecheck_only_lock_protected_merge():
+    need_gpu()
+    cmd = [_sanitizer(), "--tool", "racecheck", "--print-limit", "100000", sys.executable, TARGET]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    out = res.stdout + res.stderr
+    assert "sanitize_target done" in out, out[-4000:]
+    fns = set(re.findall(r"access at (?:surr::)?([A-Za-z_0-9]+)\(", out))
+    assert fns <= LOCKED, f"racecheck hazards outside the lock-protected top-k merge: {sorted(fns - LOCKED)}"
