@@ -206,6 +206,40 @@ uint32_t surrogate_last_launches(const surrogate_t *h);
 surr_status surrogate_selftest_umma(int cuda_device, int precision, uint32_t n, uint32_t k, const float *a_host,
                                     const float *b_host, float *d_host);
 
+/* ---------------------------------------------------------------- training
+ * GPU-side training of one F-H-H-1 FCNN, the step before
+ * the sweep: the paper's scikit-learn MLPRegressor recipe (Table
+ * "Hyperparameter" PAPER.md:212-235) in FP32 — minibatches in the given
+ * epoch orders (the last batch of an epoch short), loss 1/2 mean squared error
+ * + alpha/(2B) sum ||W||^2 (biases excluded), backpropagation with the ReLU
+ * subgradient 0 at 0, Adam with lr_t = lr0 sqrt(1 - beta2^t) / (1 - beta1^t),
+ * epoch loss = sample-weighted mean of the batch losses, stop after more than
+ * n_iter_no_change epochs without improving the best epoch loss by tol, or
+ * after max_epochs.  One launch of an H/16-CTA thread-block cluster runs the
+ * whole fit. */
+typedef struct {
+  double alpha, beta1, beta2, lr0, eps, tol; /* paper: 1e-4, 0.95, 0.90, 0.0009, 1e-9, 1e-6 */
+  uint32_t batch_size;                       /* 1..200 (paper: 200) */
+  uint32_t max_epochs;                       /* >= 1 (paper: 200) */
+  uint32_t n_iter_no_change;                 /* scikit-learn default 10 */
+} surr_train_hyper;
+
+/* widths = {F, H, H, 1} with F in 1..24 and H in {32, 64, 128}.
+ * W[l], b[l] (l = 0..2): HOST float64, row-major fan_in x fan_out; read as the
+ * initial parameters and overwritten with the trained ones.
+ * X: HOST n x F row-major, y: HOST n — already standardised (the scalers are
+ * the caller's).  perms: HOST max_epochs x n row indices (epoch e
+ * visits rows perms[e n + i] in order i; each row a permutation of 0..n-1), or
+ * NULL for the identity order every epoch.
+ * Outputs (host): loss_history[max_epochs] (epochs beyond *epochs_run are
+ * left untouched), *epochs_run, *stop_reason (0 = max_epochs, 1 = tol).
+ * Synchronous.  Errors: SURR_E_INVALID_ARG (null, n == 0, bad hyper, an index
+ * >= n in perms), SURR_E_UNSUPPORTED (widths outside the envelope). */
+surr_status surrogate_train(surrogate_t *h, const uint32_t *widths, double *const *W, double *const *b,
+                            const double *X, const double *y, uint64_t n, const uint32_t *perms,
+                            const surr_train_hyper *hyper, double *loss_history, uint32_t *epochs_run,
+                            uint32_t *stop_reason);
+
 #ifdef __cplusplus
 }
 #endif

@@ -108,8 +108,11 @@ class Adam:
         return lr_t
 
 
-def run_epochs(W, b, Xs, ys, rng, hyper=None, shuffle=True, max_epochs=None, opt=None):
+def run_epochs(W, b, Xs, ys, rng, hyper=None, shuffle=True, max_epochs=None, opt=None, perms=None):
     """The minibatch epoch loop on already-standardised data; mutates W, b.
+    perms: optional [epochs, n] epoch orders given as an input (the random
+    numbers of the shuffle passed in, so another implementation can be run on
+    the same orders); otherwise each epoch draws rng.permutation(n).
 
     Returns (loss_history, stop_reason, opt)."""
     h = dict(HYPER)
@@ -125,8 +128,10 @@ def run_epochs(W, b, Xs, ys, rng, hyper=None, shuffle=True, max_epochs=None, opt
     no_improve = 0
     reason = "max_epochs"
     idx = np.arange(n)
-    for _ in range(max_epochs if max_epochs is not None else h["max_epochs"]):
-        if shuffle:
+    for ep in range(max_epochs if max_epochs is not None else h["max_epochs"]):
+        if perms is not None:
+            idx = np.asarray(perms[ep], dtype=np.int64)
+        elif shuffle:
             idx = rng.permutation(n)
         acc = 0.0
         for s in range(0, n, bs):

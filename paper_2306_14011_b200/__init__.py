@@ -24,7 +24,7 @@ EXPORTS = [
     "surrogate_merge_topk", "surrogate_sweep_records", "surrogate_decode_range", "surrogate_space_size",
     "surrogate_kernel_timing", "surrogate_kernel_timing_get", "surrogate_last_launches",
     "surrogate_selftest_umma", "surrogate_table_bytes", "surrogate_debug_trace", "surrogate_reset_cache",
-    "surrogate_arith",
+    "surrogate_arith", "surrogate_train",
 ]
 
 
@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
         L.surrogate_debug_trace.argtypes = [vp, vp, u32]
         L.surrogate_reset_cache.argtypes = [vp]
         L.surrogate_arith.argtypes = [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_double)]
+        L.surrogate_train.argtypes = [vp, vp, vp, vp, vp, vp, u64, vp, ctypes.POINTER(_TrainHyper), vp,
+                                      ctypes.POINTER(u32), ctypes.POINTER(u32)]
         L.surrogate_table_bytes.argtypes = [vp]
         L.surrogate_table_bytes.restype = u32
         for name in EXPORTS:
@@ -311,6 +313,52 @@ def selftest_umma(precision: str, A: np.ndarray, B: np.ndarray, device: int = 0)
                                        D.ctypes.data_as(ctypes.c_void_p))
     _check(rc)
     return D
+
+
+class _TrainHyper(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("lr0", ctypes.c_double), ("eps", ctypes.c_double), ("tol", ctypes.c_double),
+                ("batch_size", ctypes.c_uint32), ("max_epochs", ctypes.c_uint32),
+                ("n_iter_no_change", ctypes.c_uint32)]
+
+
+# the paper's Table "Hyperparameter" + scikit-learn's n_iter_no_change
+TRAIN_HYPER = dict(alpha=1e-4, beta1=0.95, beta2=0.90, lr0=0.0009, eps=1e-9, tol=1e-6, batch_size=200,
+                   max_epochs=200, n_iter_no_change=10)
+
+
+def train(W, b, X, y, perms=None, hyper=None, device: int = 0):
+    """GPU training of an F-H-H-1 net (surrogate_train): W, b lists of float64
+    arrays (fan_in x fan_out, initial values; copies are returned trained), X
+    [n, F] / y [n] standardised, perms [max_epochs, n] uint32 epoch orders or
+    None.  Returns (W, b, loss_history, stop_reason in {"max_epochs", "tol_converged"})."""
+    h = dict(TRAIN_HYPER)
+    if hyper:
+        h.update(hyper)
+    W = [np.ascontiguousarray(w, np.float64).copy() for w in W]
+    b = [np.ascontiguousarray(v, np.float64).reshape(-1).copy() for v in b]
+    if len(W) != 3 or len(b) != 3:
+        raise ValueError("F-H-H-1 nets only")
+    X = np.ascontiguousarray(X, np.float64)
+    y = np.ascontiguousarray(y, np.float64).reshape(-1)
+    n = X.shape[0]
+    widths = np.ascontiguousarray([W[0].shape[0], W[0].shape[1], W[1].shape[1], W[2].shape[1]], np.uint32)
+    if perms is not None:
+        perms = np.ascontiguousarray(perms, np.uint32)
+        if perms.shape != (h["max_epochs"], n):
+            raise ValueError(f"perms must be [{h['max_epochs']}, {n}]")
+    hp = _TrainHyper(h["alpha"], h["beta1"], h["beta2"], h["lr0"], h["eps"], h["tol"], int(h["batch_size"]),
+                     int(h["max_epochs"]), int(h["n_iter_no_change"]))
+    Wp = (ctypes.c_void_p * 3)(*[w.ctypes.data for w in W])
+    bp = (ctypes.c_void_p * 3)(*[v.ctypes.data for v in b])
+    hist = np.zeros(h["max_epochs"], np.float64)
+    ep, reason = ctypes.c_uint32(), ctypes.c_uint32()
+    s = Surrogate(device)
+    _check(lib().surrogate_train(s.h, widths.ctypes.data, ctypes.cast(Wp, ctypes.c_void_p),
+                                 ctypes.cast(bp, ctypes.c_void_p), X.ctypes.data, y.ctypes.data, n,
+                                 None if perms is None else perms.ctypes.data, ctypes.byref(hp),
+                                 hist.ctypes.data, ctypes.byref(ep), ctypes.byref(reason)), s.h)
+    return W, b, hist[:ep.value].tolist(), ("tol_converged" if reason.value == 1 else "max_epochs")
 
 
 def key_to_float(keys: np.ndarray) -> np.ndarray:

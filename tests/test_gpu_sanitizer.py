@@ -40,9 +40,12 @@ def test_compute_sanitizer_clean(tool):
 # the CTA top-k list is merged by one warp at a time under a shared-memory
 # spin lock (atomicCAS acquire / atomicExch release with block fences): the
 # lock hand-off orders the warps' list accesses, but racecheck models only
-# barrier synchronisation and reports those accesses as hazards.  Every other
-# shared-memory access must be hazard-free.
-LOCKED = {"warp_merge", "upper_bound_recs_fwd", "lower_bound_recs"}
+# barrier synchronisation and reports those accesses as hazards.  topk_offer's
+# one unlocked access is the deliberate read of the CTA's current k-th key
+# (the ballot pre-filter: a stale value only admits extra candidates, the
+# locked merge keeps the exact top-k) against the lock holder's update of it.
+# Every other shared-memory access must be hazard-free.
+LOCKED = {"warp_merge", "upper_bound_recs_fwd", "lower_bound_recs", "topk_offer"}
 
 
 def test_compute_sanitizer_racecheck_only_lock_protected_merge():

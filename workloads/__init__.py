@@ -228,3 +228,41 @@ def predict_rows(value_lists, n: int, seed: int) -> np.ndarray:
     rng = np.random.default_rng([seed, 0xF00D])
     cols = [np.asarray(v, np.float64)[rng.integers(0, len(v), n)] for v in value_lists]
     return np.stack(cols, axis=1)
+
+
+# ---------------------------------------------------------------- training inputs
+# Seeded inputs of the GPU-training parity tests: both the
+# oracle and the CUDA trainer receive the same initial weights (glorot_init),
+# the same standardised data (training_rows) and the same epoch orders
+# (epoch_permutations); nothing here is the method's arithmetic.
+
+def glorot_init(widths, seed: int):
+    """Glorot-uniform U(+-sqrt(6/(fan_in+fan_out))) weights and biases (the
+    scikit-learn initialisation the paper's MLPRegressor uses)."""
+    rng = np.random.default_rng([seed, 0x61])
+    W, b = [], []
+    for fi, fo in zip(widths[:-1], widths[1:]):
+        bound = np.sqrt(6.0 / (fi + fo))
+        W.append(rng.uniform(-bound, bound, (fi, fo)))
+        b.append(rng.uniform(-bound, bound, fo))
+    return W, b
+
+
+def training_rows(value_lists, n: int, seed: int, noise: float = 0.02):
+    """n random configs and a smooth synthetic runtime (a sum of log2-quadratic
+    bowls plus Gaussian noise), both standardised column-wise: (Xs [n, P], ys [n])."""
+    X = predict_rows(value_lists, n, seed)
+    rng = np.random.default_rng([seed, 0x7A])
+    L = np.log2(X)
+    opt = np.array([rng.uniform(np.log2(min(v)), np.log2(max(v))) for v in value_lists])
+    a = rng.uniform(0.02, 0.1, len(value_lists))
+    y = 1.0 + ((L - opt) ** 2 * a).sum(axis=1) + noise * rng.standard_normal(n)
+    Xs = (X - X.mean(axis=0)) / np.where(X.std(axis=0) > 0, X.std(axis=0), 1.0)
+    ys = (y - y.mean()) / y.std()
+    return Xs, ys
+
+
+def epoch_permutations(n: int, epochs: int, seed: int) -> np.ndarray:
+    """[epochs, n] uint32: one seeded permutation of 0..n-1 per epoch."""
+    rng = np.random.default_rng([seed, 0x5EF])
+    return np.stack([rng.permutation(n) for _ in range(epochs)]).astype(np.uint32)
