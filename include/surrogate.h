@@ -224,18 +224,22 @@ typedef struct {
   uint32_t n_iter_no_change;                 /* scikit-learn default 10 */
 } surr_train_hyper;
 
-/* widths = {F, H, H, 1} with F in 1..24 and H in {32, 64, 128}.
- * W[l], b[l] (l = 0..2): HOST float64, row-major fan_in x fan_out; read as the
- * initial parameters and overwritten with the trained ones.
+/* widths = {F, H, H, 1} with F in 1..20 and H in {32, 64, 128}; E >= 1
+ * ensemble members trained at once on the same data, each with
+ * its own initial values and epoch orders (one cluster per member).
+ * W[3 e + l], b[3 e + l] (l = 0..2): HOST float64, row-major fan_in x fan_out;
+ * read as member e's initial parameters and overwritten with the trained ones.
  * X: HOST n x F row-major, y: HOST n — already standardised (the scalers are
- * the caller's).  perms: HOST max_epochs x n row indices (epoch e
- * visits rows perms[e n + i] in order i; each row a permutation of 0..n-1), or
- * NULL for the identity order every epoch.
- * Outputs (host): loss_history[max_epochs] (epochs beyond *epochs_run are
- * left untouched), *epochs_run, *stop_reason (0 = max_epochs, 1 = tol).
- * Synchronous.  Errors: SURR_E_INVALID_ARG (null, n == 0, bad hyper, an index
- * >= n in perms), SURR_E_UNSUPPORTED (widths outside the envelope). */
-surr_status surrogate_train(surrogate_t *h, const uint32_t *widths, double *const *W, double *const *b,
+ * the caller's).  perms: HOST E x max_epochs x n row indices
+ * (member e, epoch p visits rows perms[(e max_epochs + p) n + i] in order i;
+ * each row a permutation of 0..n-1), or NULL for the identity order.
+ * Outputs (host): loss_history[E x max_epochs] (epochs beyond a member's
+ * epochs_run left untouched), epochs_run[E], stop_reason[E] (0 = max_epochs,
+ * 1 = tol).  Synchronous.  Errors: SURR_E_INVALID_ARG (null, n == 0, E == 0,
+ * bad hyper, an index >= n in perms), SURR_E_UNSUPPORTED (widths outside the
+ * envelope).  Members are independent clusters: more than fit at once run in
+ * further waves. */
+surr_status surrogate_train(surrogate_t *h, const uint32_t *widths, uint32_t E, double *const *W, double *const *b,
                             const double *X, const double *y, uint64_t n, const uint32_t *perms,
                             const surr_train_hyper *hyper, double *loss_history, uint32_t *epochs_run,
                             uint32_t *stop_reason);

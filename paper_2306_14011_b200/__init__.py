@@ -82,8 +82,7 @@ def lib() -> ctypes.CDLL:
         L.surrogate_debug_trace.argtypes = [vp, vp, u32]
         L.surrogate_reset_cache.argtypes = [vp]
         L.surrogate_arith.argtypes = [vp, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_double)]
-        L.surrogate_train.argtypes = [vp, vp, vp, vp, vp, vp, u64, vp, ctypes.POINTER(_TrainHyper), vp,
-                                      ctypes.POINTER(u32), ctypes.POINTER(u32)]
+        L.surrogate_train.argtypes = [vp, vp, u32, vp, vp, vp, vp, u64, vp, ctypes.POINTER(_TrainHyper), vp, vp, vp]
         L.surrogate_table_bytes.argtypes = [vp]
         L.surrogate_table_bytes.restype = u32
         for name in EXPORTS:
@@ -327,38 +326,48 @@ TRAIN_HYPER = dict(alpha=1e-4, beta1=0.95, beta2=0.90, lr0=0.0009, eps=1e-9, tol
                    max_epochs=200, n_iter_no_change=10)
 
 
-def train(W, b, X, y, perms=None, hyper=None, device: int = 0):
-    """GPU training of an F-H-H-1 net (surrogate_train): W, b lists of float64
-    arrays (fan_in x fan_out, initial values; copies are returned trained), X
-    [n, F] / y [n] standardised, perms [max_epochs, n] uint32 epoch orders or
-    None.  Returns (W, b, loss_history, stop_reason in {"max_epochs", "tol_converged"})."""
+def train_ensemble(members, X, y, perms=None, hyper=None, device: int = 0):
+    """GPU training of E F-H-H-1 nets at once (surrogate_train, one cluster per
+    member): members = [(W, b), ...] with W, b lists of 3 float64 arrays
+    (fan_in x fan_out, initial values); X [n, F] / y [n] standardised; perms
+    [E, max_epochs, n] uint32 epoch orders or None.  Returns, per member,
+    (W, b, loss_history, stop_reason in {"max_epochs", "tol_converged"})."""
     h = dict(TRAIN_HYPER)
     if hyper:
         h.update(hyper)
-    W = [np.ascontiguousarray(w, np.float64).copy() for w in W]
-    b = [np.ascontiguousarray(v, np.float64).reshape(-1).copy() for v in b]
-    if len(W) != 3 or len(b) != 3:
-        raise ValueError("F-H-H-1 nets only")
+    E = len(members)
+    Ws = [[np.ascontiguousarray(w, np.float64).copy() for w in m[0]] for m in members]
+    bs = [[np.ascontiguousarray(v, np.float64).reshape(-1).copy() for v in m[1]] for m in members]
+    if E == 0 or any(len(w) != 3 or len(v) != 3 for w, v in zip(Ws, bs)):
+        raise ValueError("one or more F-H-H-1 nets")
     X = np.ascontiguousarray(X, np.float64)
     y = np.ascontiguousarray(y, np.float64).reshape(-1)
     n = X.shape[0]
-    widths = np.ascontiguousarray([W[0].shape[0], W[0].shape[1], W[1].shape[1], W[2].shape[1]], np.uint32)
+    W0 = Ws[0]
+    widths = np.ascontiguousarray([W0[0].shape[0], W0[0].shape[1], W0[1].shape[1], W0[2].shape[1]], np.uint32)
     if perms is not None:
         perms = np.ascontiguousarray(perms, np.uint32)
-        if perms.shape != (h["max_epochs"], n):
-            raise ValueError(f"perms must be [{h['max_epochs']}, {n}]")
+        if perms.shape != (E, h["max_epochs"], n):
+            raise ValueError(f"perms must be [{E}, {h['max_epochs']}, {n}]")
     hp = _TrainHyper(h["alpha"], h["beta1"], h["beta2"], h["lr0"], h["eps"], h["tol"], int(h["batch_size"]),
                      int(h["max_epochs"]), int(h["n_iter_no_change"]))
-    Wp = (ctypes.c_void_p * 3)(*[w.ctypes.data for w in W])
-    bp = (ctypes.c_void_p * 3)(*[v.ctypes.data for v in b])
-    hist = np.zeros(h["max_epochs"], np.float64)
-    ep, reason = ctypes.c_uint32(), ctypes.c_uint32()
+    Wp = (ctypes.c_void_p * (3 * E))(*[w.ctypes.data for m in Ws for w in m])
+    bp = (ctypes.c_void_p * (3 * E))(*[v.ctypes.data for m in bs for v in m])
+    hist = np.zeros((E, h["max_epochs"]), np.float64)
+    ep = np.zeros(E, np.uint32)
+    reason = np.zeros(E, np.uint32)
     s = Surrogate(device)
-    _check(lib().surrogate_train(s.h, widths.ctypes.data, ctypes.cast(Wp, ctypes.c_void_p),
+    _check(lib().surrogate_train(s.h, widths.ctypes.data, E, ctypes.cast(Wp, ctypes.c_void_p),
                                  ctypes.cast(bp, ctypes.c_void_p), X.ctypes.data, y.ctypes.data, n,
                                  None if perms is None else perms.ctypes.data, ctypes.byref(hp),
-                                 hist.ctypes.data, ctypes.byref(ep), ctypes.byref(reason)), s.h)
-    return W, b, hist[:ep.value].tolist(), ("tol_converged" if reason.value == 1 else "max_epochs")
+                                 hist.ctypes.data, ep.ctypes.data, reason.ctypes.data), s.h)
+    return [(Ws[e], bs[e], hist[e, :ep[e]].tolist(), "tol_converged" if reason[e] == 1 else "max_epochs")
+            for e in range(E)]
+
+
+def train(W, b, X, y, perms=None, hyper=None, device: int = 0):
+    """One member: train_ensemble([(W, b)], ...) with perms [max_epochs, n]."""
+    return train_ensemble([(W, b)], X, y, None if perms is None else np.asarray(perms)[None], hyper, device)[0]
 
 
 def key_to_float(keys: np.ndarray) -> np.ndarray:

@@ -1152,48 +1152,56 @@ surr_status surrogate_selftest_umma(int cuda_device, int precision, uint32_t n, 
   return SURR_OK;
 }
 
-surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, double* const* W, double* const* b,
+surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, uint32_t E, double* const* W, double* const* b,
                             const double* X, const double* y, uint64_t n, const uint32_t* perms,
                             const surr_train_hyper* hy, double* loss_history, uint32_t* epochs_run,
                             uint32_t* stop_reason) {
   if (!h || !widths || !W || !b || !X || !y || !hy || !loss_history || !epochs_run || !stop_reason)
     return fail(h, SURR_E_INVALID_ARG, "null argument");
-  for (int l = 0; l < 3; ++l)
-    if (!W[l] || !b[l]) return fail(h, SURR_E_INVALID_ARG, "null layer %d", l);
+  if (E == 0) return fail(h, SURR_E_INVALID_ARG, "E == 0");
+  for (uint32_t l = 0; l < 3 * E; ++l)
+    if (!W[l] || !b[l]) return fail(h, SURR_E_INVALID_ARG, "null layer %u", l);
   const uint32_t F = widths[0], H = widths[1];
   if (widths[2] != H || widths[3] != 1)
     return fail(h, SURR_E_UNSUPPORTED, "training supports F-H-H-1 nets (two equal hidden layers)");
   if (F < 1 || F > (uint32_t)TR_FMAX) return fail(h, SURR_E_UNSUPPORTED, "F = %u outside 1..%d", F, TR_FMAX);
   if (H != 32 && H != 64 && H != 128) return fail(h, SURR_E_UNSUPPORTED, "H = %u not in {32, 64, 128}", H);
+  const uint32_t C = H / TR_CPC;
   if (n == 0 || n > 0xFFFFFFFFull) return fail(h, SURR_E_INVALID_ARG, "n = %llu", (unsigned long long)n);
   if (hy->batch_size < 1 || hy->batch_size > (uint32_t)TR_BMAX || hy->max_epochs < 1 || !(hy->lr0 > 0.0) ||
       !(hy->beta1 >= 0.0 && hy->beta1 < 1.0) || !(hy->beta2 >= 0.0 && hy->beta2 < 1.0) || !(hy->eps > 0.0) ||
       !(hy->alpha >= 0.0))
     return fail(h, SURR_E_INVALID_ARG, "hyperparameters outside their domain");
+  const uint64_t nperm = (uint64_t)E * hy->max_epochs * n;
   if (perms)
-    for (uint64_t i = 0; i < (uint64_t)hy->max_epochs * n; ++i)
+    for (uint64_t i = 0; i < nperm; ++i)
       if (perms[i] >= n) return fail(h, SURR_E_INVALID_ARG, "perms[%llu] = %u >= n", (unsigned long long)i, perms[i]);
   CU(cudaSetDevice(h->dev));
+  // member image: W1 [F][H], b1, W2 [H][H], b2, W3 [H], b3, padded to 4 floats
   const size_t sizes[6] = {(size_t)F * H, H, (size_t)H * H, H, H, 1};
-  const double* src[6] = {W[0], b[0], W[1], b[1], W[2], b[2]};
   size_t off[7] = {0};
   for (int i = 0; i < 6; ++i) off[i + 1] = off[i] + sizes[i];
-  const uint32_t C = H / TR_CPC;
-  std::vector<float> hp(off[6]), hx((size_t)n * F), hyv(n);
-  for (int i = 0; i < 6; ++i)
-    for (size_t j = 0; j < sizes[i]; ++j) hp[off[i] + j] = (float)src[i][j];
+  const size_t pstride = align_up(off[6], 4);
+  std::vector<float> hp(pstride * E, 0.0f), hx((size_t)n * F), hyv(n);
+  for (uint32_t e = 0; e < E; ++e)
+    for (int i = 0; i < 6; ++i) {
+      const double* src = (i % 2 == 0) ? W[3 * e + i / 2] : b[3 * e + i / 2];
+      for (size_t j = 0; j < sizes[i]; ++j) hp[e * pstride + off[i] + j] = (float)src[j];
+    }
   for (size_t i = 0; i < (size_t)n * F; ++i) hx[i] = (float)X[i];
   for (uint64_t i = 0; i < n; ++i) hyv[i] = (float)y[i];
   float *dp = nullptr, *dx = nullptr, *dy = nullptr, *dmv = nullptr;
   uint32_t *dperm = nullptr, *dres = nullptr;
   double* dloss = nullptr;
-  const size_t perm_bytes = perms ? (size_t)hy->max_epochs * n * 4 : 0;
+  const size_t perm_bytes = perms ? nperm * 4 : 0;
   auto release = [&]() {
     cudaFree(dp); cudaFree(dx); cudaFree(dy); cudaFree(dmv); cudaFree(dperm); cudaFree(dres); cudaFree(dloss);
   };
-  if (cudaMalloc(&dp, off[6] * 4) != cudaSuccess || cudaMalloc(&dx, hx.size() * 4) != cudaSuccess ||
-      cudaMalloc(&dy, hyv.size() * 4) != cudaSuccess || cudaMalloc(&dmv, (size_t)C * 2 * H * TR_CPC * 4) != cudaSuccess ||
-      cudaMalloc(&dres, 16) != cudaSuccess || cudaMalloc(&dloss, (size_t)hy->max_epochs * 8) != cudaSuccess ||
+  if (cudaMalloc(&dp, hp.size() * 4) != cudaSuccess || cudaMalloc(&dx, hx.size() * 4) != cudaSuccess ||
+      cudaMalloc(&dy, hyv.size() * 4) != cudaSuccess ||
+      cudaMalloc(&dmv, (size_t)E * C * 2 * H * TR_CPC * 4) != cudaSuccess ||
+      cudaMalloc(&dres, (size_t)E * 12) != cudaSuccess ||
+      cudaMalloc(&dloss, (size_t)E * hy->max_epochs * 8) != cudaSuccess ||
       (perms && cudaMalloc(&dperm, perm_bytes) != cudaSuccess)) {
     release();
     return fail(h, SURR_E_OOM, "cudaMalloc (training buffers)");
@@ -1205,18 +1213,20 @@ surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, double* cons
     cudaError_t e_ = (call);                                                               \
     if (e_ != cudaSuccess) { rc = fail(h, SURR_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); break; } \
   }
-    TCU(cudaMemcpy(dp, hp.data(), off[6] * 4, cudaMemcpyHostToDevice));
+    TCU(cudaMemcpy(dp, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice));
     TCU(cudaMemcpy(dx, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice));
     TCU(cudaMemcpy(dy, hyv.data(), hyv.size() * 4, cudaMemcpyHostToDevice));
     if (perms) TCU(cudaMemcpy(dperm, perms, perm_bytes, cudaMemcpyHostToDevice));
     TrainParams tp{};
     tp.X = dx; tp.y = dy; tp.perms = dperm;
-    tp.n = (uint32_t)n; tp.F = F; tp.B = hy->batch_size;
+    tp.n = (uint32_t)n; tp.F = F; tp.B = hy->batch_size; tp.E = E;
     tp.max_epochs = hy->max_epochs; tp.n_iter_no_change = hy->n_iter_no_change;
     tp.alpha = (float)hy->alpha; tp.beta1 = (float)hy->beta1; tp.beta2 = (float)hy->beta2;
     tp.lr0 = (float)hy->lr0; tp.eps = (float)hy->eps; tp.tol = hy->tol;
-    tp.W1 = dp + off[0]; tp.b1 = dp + off[1]; tp.W2 = dp + off[2]; tp.b2 = dp + off[3]; tp.W3 = dp + off[4];
-    tp.b3 = dp + off[5];
+    tp.params = dp;
+    tp.pstride = (uint32_t)pstride;
+    tp.oW1 = (uint32_t)off[0]; tp.ob1 = (uint32_t)off[1]; tp.oW2 = (uint32_t)off[2];
+    tp.ob2 = (uint32_t)off[3]; tp.oW3 = (uint32_t)off[4]; tp.ob3 = (uint32_t)off[5];
     tp.mv = dmv; tp.loss_hist = dloss; tp.result = dres;
     const void* fn = H == 32 ? (const void*)&train_kernel<32> : H == 64 ? (const void*)&train_kernel<64>
                                                                         : (const void*)&train_kernel<128>;
@@ -1224,7 +1234,7 @@ surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, double* cons
     if (smem > SMEM_MAX) { rc = fail(h, SURR_E_UNSUPPORTED, "training shared memory %zu B", smem); break; }
     TCU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(C, 1, 1);
+    cfg.gridDim = dim3(C * E, 1, 1);
     cfg.blockDim = dim3(TR_THREADS, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = nullptr;
@@ -1239,16 +1249,21 @@ surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, double* cons
     TCU(cudaLaunchKernelExC(&cfg, fn, args));
     h->launches = 1;
     TCU(cudaDeviceSynchronize());
-    uint32_t res[3];
-    TCU(cudaMemcpy(res, dres, 12, cudaMemcpyDeviceToHost));
-    TCU(cudaMemcpy(hp.data(), dp, off[6] * 4, cudaMemcpyDeviceToHost));
-    std::vector<double> lh(hy->max_epochs);
-    TCU(cudaMemcpy(lh.data(), dloss, (size_t)res[0] * 8, cudaMemcpyDeviceToHost));
-    for (uint32_t e = 0; e < res[0]; ++e) loss_history[e] = lh[e];
-    for (int i = 0; i < 6; ++i)
-      for (size_t j = 0; j < sizes[i]; ++j) const_cast<double*>(src[i])[j] = (double)hp[off[i] + j];
-    *epochs_run = res[0];
-    *stop_reason = res[1];
+    std::vector<uint32_t> res((size_t)E * 3);
+    TCU(cudaMemcpy(res.data(), dres, res.size() * 4, cudaMemcpyDeviceToHost));
+    TCU(cudaMemcpy(hp.data(), dp, hp.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<double> lh((size_t)E * hy->max_epochs);
+    TCU(cudaMemcpy(lh.data(), dloss, lh.size() * 8, cudaMemcpyDeviceToHost));
+    for (uint32_t e = 0; e < E; ++e) {
+      for (uint32_t p = 0; p < res[3 * e]; ++p)
+        loss_history[(size_t)e * hy->max_epochs + p] = lh[(size_t)e * hy->max_epochs + p];
+      for (int i = 0; i < 6; ++i) {
+        double* dst = (i % 2 == 0) ? W[3 * e + i / 2] : b[3 * e + i / 2];
+        for (size_t j = 0; j < sizes[i]; ++j) dst[j] = (double)hp[e * pstride + off[i] + j];
+      }
+      epochs_run[e] = res[3 * e];
+      stop_reason[e] = res[3 * e + 1];
+    }
 #undef TCU
   } while (0);
   release();

@@ -90,3 +90,23 @@ def test_train_rejects_bad_input():
         pk.train(W0, b0, X, y, bad, dict(HYPER, max_epochs=2))
     with pytest.raises(pk.SurrogateError):
         pk.train(W0, b0, X, y, None, dict(HYPER, max_epochs=2, batch_size=512))
+
+
+def test_train_ensemble_members_independent_and_bitwise():
+    # E clusters in one launch: each member equals its own single-member fit bitwise,
+    # and member 1's first steps match the oracle on its own inputs
+    pk = need_gpu()
+    vl = workloads.space("cfg2")
+    n, E, ep = 700, 3, 2
+    X, y = workloads.training_rows(vl, n, seed=21)
+    inits = [workloads.glorot_init([14, 32, 32, 1], seed=30 + e) for e in range(E)]
+    perms = np.stack([workloads.epoch_permutations(n, ep, seed=40 + e) for e in range(E)])
+    res = pk.train_ensemble(inits, X, y, perms, dict(HYPER, max_epochs=ep))
+    for e in range(E):
+        We, be, he, _ = pk.train(inits[e][0], inits[e][1], X, y, perms[e], dict(HYPER, max_epochs=ep))
+        assert all(np.array_equal(a, c) for a, c in zip(res[e][0] + res[e][1], We + be))
+        assert res[e][2] == he
+    Wo, bo, ho, _ = _oracle(inits[1][0], inits[1][1], X, y, perms[1], ep)
+    assert np.allclose(res[1][2], ho, rtol=1e-5, atol=0.0)
+    err = max(np.abs(a - c).max() for a, c in zip(res[1][0] + res[1][1], Wo + bo))
+    assert err <= 1e-5 * ep * 4 * 0.0009 + 4e-7 * 3

@@ -209,3 +209,21 @@ def test_predict_row_purity_and_ensemble_mean():
     assert np.array_equal(mlp.predict(model, X[perm]), t[perm])
     one = [dict(model, members=[m]) for m in model["members"]]
     assert np.allclose(t, (mlp.predict(one[0], X) + mlp.predict(one[1], X)) / 2, rtol=0, atol=1e-15)
+
+
+def test_run_epochs_given_orders_equal_drawn_orders():
+    # passing the epoch orders as an input (the GPU-training parity path) is the
+    # same computation as drawing them from the rng inside the loop
+    rng = np.random.default_rng(42)
+    X = rng.standard_normal((450, 5))
+    y = rng.standard_normal(450)
+    W0, b0 = mlp.init_glorot([5, 8, 8, 1], np.random.default_rng(1))
+    r1 = np.random.default_rng(9)
+    W1, b1 = [w.copy() for w in W0], [v.copy() for v in b0]
+    h1, _, _ = mlp.run_epochs(W1, b1, X, y, r1, max_epochs=4)
+    r2 = np.random.default_rng(9)
+    perms = [r2.permutation(450) for _ in range(4)]
+    W2, b2 = [w.copy() for w in W0], [v.copy() for v in b0]
+    h2, _, _ = mlp.run_epochs(W2, b2, X, y, None, max_epochs=4, perms=perms)
+    assert h1 == h2
+    assert all(np.array_equal(a, c) for a, c in zip(W1 + b1, W2 + b2))
