@@ -22,6 +22,7 @@
 #include "sweep_kernel.cuh"
 #include "sweep_kernel3.cuh"
 #include "sweep_kernel5.cuh"
+#include "sweep_kernel6.cuh"
 #include "sweep_kernel_pair.cuh"
 #include "train_kernel.cuh"
 #ifndef SURR_PAIR_NSUB
@@ -208,6 +209,15 @@ KernelInfo kinfo5() {
   return ki;
 }
 
+template <int H>
+KernelInfo kinfo6() {
+  using C = Cfg6<H>;
+  KernelInfo ki{(const void*)&sweep_kernel6<H>, C::NSLOT, C::THREADS, false};
+  ki.a0_smem = true;  // A0 hi / lo tiles per slot
+  ki.a0_tiles = 2;
+  return ki;
+}
+
 template <int PREC, int H>
 KernelInfo kinfo() {
   using C = Cfg<PREC, H>;
@@ -267,6 +277,16 @@ bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg 
   // FP32 (3xTF32) nets with at most one hidden->hidden layer: self-issuing, split
   // columns, separate D2 region (measured faster than the general kernel; for
   // 1xTF32 the general two-slot kernel measured faster, 572 vs 482 TFLOP/s)
+  // FP32 path as 3xFP16 with a hidden->hidden layer: three slots sharing the
+  // last-layer region (SURR_VARIANT=9 selects the two-slot kernel for A/B runs)
+  if (prec == PREC_FP32H && NL == 2) {
+    const char* v = getenv("SURR_VARIANT");
+    if (!(v && atoi(v) == 9)) {
+      if (H == 32) { *ki = kinfo6<32>(); return true; }
+      if (H == 64) { *ki = kinfo6<64>(); return true; }
+      if (H == 128) { *ki = kinfo6<128>(); return true; }
+    }
+  }
   if ((prec == PREC_FP32 || prec == PREC_FP32H) && NL <= 2) {
 #define CASE5(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo5<P_, H_>(); return true; }

@@ -396,3 +396,43 @@ def test_shallow_and_narrow_nets(pk, prec, hidden):
     ri, rt = osweep.topk(model, vl, 32, 1_000_003, 1_000_003 + 300_000)
     check_topk(idx.cpu().numpy().astype(np.uint64), tk.cpu().numpy(), ri, rt,
                lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, bench launch configuration
+def _full_sweep_checks(pk, model, vl, prec, k, sample_seed):
+    """Full-space sweep as bench.py runs it: every returned item re-evaluated by
+    the oracle (within tol, sorted), and a property that holds at any size: no
+    sampled config the top-k left out is faster than the k-th time by more than
+    the tie band."""
+    h = _handle(pk, model, prec)
+    idx, t, cnt = h.sweep(vl, k)
+    idx = idx.cpu().numpy().astype(np.uint64)
+    t = t.cpu().numpy()
+    assert cnt == k and np.all(np.diff(t) >= 0) and len(set(idx.tolist())) == k
+    assert rel_err(t, osweep.times_at(model, vl, idx), model["y_scale"]).max() <= TOL[prec]
+    N = int(np.prod([len(v) for v in vl]))
+    rng = np.random.default_rng(sample_seed)
+    sample = np.unique(rng.integers(0, N, 1 << 17, dtype=np.uint64))
+    ts = osweep.times_at(model, vl, sample)
+    Tk = float(t[-1])
+    band = 2 * TOL[prec] * abs(Tk)
+    missing = sample[(ts < Tk - band) & ~np.isin(sample, idx)]
+    assert missing.size == 0, f"{missing.size} sampled configs faster than the k-th time are not in the top-k"
+
+
+@pytest.mark.parametrize("prec", ["fp16", "fp32"])
+def test_cfg5_full_sweep_reevaluated_and_sampled(pk, prec):
+    vl = workloads.space("cfg5")
+    _full_sweep_checks(pk, workloads.load_model("cfg5_14-128-128-1"), vl, prec, 1024, 5)
+
+
+def test_cfg4_full_sweep_reevaluated_and_sampled(pk):
+    vl = workloads.space("cfg2")
+    model = workloads.with_device(workloads.load_model("cfg4_17-128-128-1_x8"),
+                                  workloads.device_features("onehot", "V100"))
+    _full_sweep_checks(pk, model, vl, "fp16", 16, 4)
+
+
+def test_cfg2_full_sweep_sampled_property(pk):
+    vl = workloads.space("cfg2")
+    _full_sweep_checks(pk, workloads.load_model("cfg2_14-128-128-1"), vl, "fp16", 16, 2)
