@@ -1248,6 +1248,11 @@ surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, uint32_t E, 
     tp.oW1 = (uint32_t)off[0]; tp.ob1 = (uint32_t)off[1]; tp.oW2 = (uint32_t)off[2];
     tp.ob2 = (uint32_t)off[3]; tp.oW3 = (uint32_t)off[4]; tp.ob3 = (uint32_t)off[5];
     tp.mv = dmv; tp.loss_hist = dloss; tp.result = dres;
+    unsigned long long* dprof = nullptr;  // development: SURR_TRAIN_PROF=1 prints per-phase cycles
+    if (getenv("SURR_TRAIN_PROF") && cudaMalloc(&dprof, 16 * 8) == cudaSuccess) {
+      cudaMemset(dprof, 0, 16 * 8);
+      tp.prof = dprof;
+    }
     const void* fn = H == 32 ? (const void*)&train_kernel<32> : H == 64 ? (const void*)&train_kernel<64>
                                                                         : (const void*)&train_kernel<128>;
     const size_t smem = H == 32 ? sizeof(TrainSmem<32>) : H == 64 ? sizeof(TrainSmem<64>) : sizeof(TrainSmem<128>);
@@ -1269,6 +1274,14 @@ surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, uint32_t E, 
     TCU(cudaLaunchKernelExC(&cfg, fn, args));
     h->launches = 1;
     TCU(cudaDeviceSynchronize());
+    if (dprof) {
+      unsigned long long pr[16];
+      cudaMemcpy(pr, dprof, sizeof pr, cudaMemcpyDeviceToHost);
+      cudaFree(dprof);
+      fprintf(stderr, "train phases (cycles, CTA 0):");
+      for (int i = 0; i < 14; ++i) fprintf(stderr, " %d:%llu", i, pr[i]);
+      fprintf(stderr, "\n");
+    }
     std::vector<uint32_t> res((size_t)E * 3);
     TCU(cudaMemcpy(res.data(), dres, res.size() * 4, cudaMemcpyDeviceToHost));
     TCU(cudaMemcpy(hp.data(), dp, hp.size() * 4, cudaMemcpyDeviceToHost));

@@ -59,6 +59,7 @@ struct TrainParams {
   float* mv;              // Adam moments of the W2 columns: [E][C][2][H][16]
   double* loss_hist;      // [E][max_epochs]
   uint32_t* result;       // [E][3]: epochs run, stop reason (0 max_epochs, 1 tol), Adam steps
+  unsigned long long* prof;  // development: per-phase clock64 sums of CTA 0 thread 0 (null: off)
 };
 
 template <int H>
@@ -135,6 +136,34 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
   float* mW2 = p.mv + ((size_t)e * C + c) * 2 * H * TR_CPC;
   float* vW2 = mW2 + H * TR_CPC;
   const uint32_t* perms = p.perms ? p.perms + (size_t)e * p.max_epochs * p.n : nullptr;
+  unsigned long long* prof = (p.prof && blockIdx.x == 0 && tid == 0) ? p.prof : nullptr;
+  long long tmark = 0;
+  // copy the other CTAs' 16-unit slices of AT (rows [16 q, 16 q + 16), B4 columns)
+  // into ours: thread = (unit j = tid / 16, 16-byte words tid % 16 + 16 u); a
+  // remote slice's four DSMEM loads are in flight before their stores
+  auto gather = [&](int B4) {
+    const int j = tid >> 4, w0 = (tid & 15) * 4;
+#pragma unroll 1
+    for (int q = 1; q < C; ++q) {
+      const int rc = (c + q) % C;
+      const float* src = cluster.map_shared_rank(s.AT, rc) + (rc * TR_CPC + j) * BM;
+      float* dst = s.AT + (rc * TR_CPC + j) * BM;
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (w0 + 64 * u < B4) v[u] = ld4(src + w0 + 64 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (w0 + 64 * u < B4) *reinterpret_cast<float4*>(dst + w0 + 64 * u) = v[u];
+    }
+  };
+  auto mark = [&](int i) {  // phase i ended now
+    if (prof) {
+      const long long now = clock64();
+      if (i >= 0) prof[i] += (unsigned long long)(now - tmark);
+      tmark = now;
+    }
+  };
 
   // ---- initial parameters (own columns, full W2), zero moments and padding rows
   for (int i = tid; i < H * H; i += TR_THREADS) s.W2[(i / H) * WS + i % H] = gW2p[i];
@@ -162,6 +191,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
   for (int i = tid; i < H * BM; i += TR_THREADS) s.AT[i] = 0.0f;
   for (int i = tid; i < TR_CPC * BM; i += TR_THREADS) s.h1T[i] = s.h2T[i] = 0.0f;
   cluster.sync();
+  mark(-1);
 
   const float alpha = p.alpha;
   double best = 1.0 / 0.0;
@@ -178,13 +208,21 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
       // ---- batch rows -> shared memory (unit-major); zero the tail rows of a short batch
       for (int r = tid; r < B; r += TR_THREADS) idx[r] = perm ? perm[s0 + r] : s0 + r;
       __syncthreads();
-      for (int i = tid; i < B * F; i += TR_THREADS) {
-        const int r = i / F, f = i % F;
-        s.XT[f * BM + r] = p.X[(size_t)idx[r] * F + f];
+      for (int r = tid; r < B; r += TR_THREADS) {  // one row per thread: F loads in flight
+        const float* xr = p.X + (size_t)idx[r] * F;
+        float xv[TR_FMAX];
+#pragma unroll
+        for (int f = 0; f < TR_FMAX; ++f)
+          if (f < F) xv[f] = __ldg(xr + f);
+        const float yv = __ldg(p.y + idx[r]);
+#pragma unroll
+        for (int f = 0; f < TR_FMAX; ++f)
+          if (f < F) s.XT[f * BM + r] = xv[f];
+        s.y[r] = yv;
       }
       for (int i = tid; i < (B4 - B) * F; i += TR_THREADS) s.XT[(i % F) * BM + B + i / F] = 0.0f;
-      for (int r = tid; r < B; r += TR_THREADS) s.y[r] = p.y[idx[r]];
       __syncthreads();
+      mark(0);
 
       // ---- forward, layer 1 (own units): h1 = relu(X W1 + b1) -> h1T and AT[own]
       for (int tt = tid; tt < (B4 / 4) * (TR_CPC / 4); tt += TR_THREADS) {
@@ -218,17 +256,12 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
         q = block_sum(q, s.red);
         if (tid == 0) s.wsq = q;
       }
+      mark(1);
       cluster.sync();  // (1) every CTA's h1 slice is written
-      for (int q = 1; q < C; ++q) {  // gather the other CTAs' h1 units (16-byte DSMEM loads)
-        const int rc = (c + q) % C;
-        const float* rA = cluster.map_shared_rank(s.AT, rc) + rc * TR_CPC * BM;
-        float* lA = s.AT + rc * TR_CPC * BM;
-        for (int i = tid; i < TR_CPC * (B4 / 4); i += TR_THREADS) {
-          const int o = (i / (B4 / 4)) * BM + (i % (B4 / 4)) * 4;
-          *reinterpret_cast<float4*>(&lA[o]) = ld4(&rA[o]);
-        }
-      }
+      mark(2);
+      gather(B4);  // the other CTAs' h1 units
       __syncthreads();
+      mark(3);
 
       // ---- forward, layer 2 (own units): h2 = relu(h1 W2 + b2); partial output h2 . W3
       for (int tt = tid; tt < (B4 / 4) * (TR_CPC / 4); tt += TR_THREADS) {
@@ -257,7 +290,9 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
         for (int j = 0; j < TR_CPC; ++j) a = fmaf(s.h2T[j * BM + r], s.W3o[j], a);
         s.ypart[r] = a;
       }
+      mark(4);
       cluster.sync();  // (2) every CTA's partial output and weight norm are written
+      mark(5);
 
       // ---- output and loss (every CTA, same order): yhat = b3 + sum_q ypart_q
       float wsq = 0.0f;
@@ -276,6 +311,7 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
       l2 = block_sum(l2, s.red);  // includes __syncthreads: d3 visible
       const float loss = 0.5f * l2 * invB + 0.5f * alpha * wsq * invB;
       acc += (double)loss * (double)B;
+      mark(6);
 
       // ---- backward: gW3 (warp w: units w, w + 8), gb3; d2 = d3 W3 . [h2 > 0] in place
       {
@@ -304,14 +340,16 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
       __syncthreads();
       // gW2[:, own] = (h1^T d2 + alpha W2) / B (AT still holds h1): thread tile 2 k x 4 j
       {
-        const int k0 = (tid >> 2) * 2, j0 = (tid & 3) * 4;
+        // units j = q + 4 v (q = tid % 4): the 4 threads of a quarter-warp read
+        // consecutive h2T rows, whose 16-byte words fall in distinct bank groups
+        const int k0 = (tid >> 2) * 2, q4 = tid & 3;
         if (k0 < H) {
           float a[2][4] = {};
           for (int r = 0; r < B4; r += 4) {
             const float4 x0 = ld4(&s.AT[k0 * BM + r]), x1 = ld4(&s.AT[(k0 + 1) * BM + r]);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-              const float4 d = ld4(&s.h2T[(j0 + v) * BM + r]);
+              const float4 d = ld4(&s.h2T[(q4 + 4 * v) * BM + r]);
               a[0][v] = fmaf(x0.x, d.x, fmaf(x0.y, d.y, fmaf(x0.z, d.z, fmaf(x0.w, d.w, a[0][v]))));
               a[1][v] = fmaf(x1.x, d.x, fmaf(x1.y, d.y, fmaf(x1.z, d.z, fmaf(x1.w, d.w, a[1][v]))));
             }
@@ -320,13 +358,18 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
           for (int u = 0; u < 2; ++u)
 #pragma unroll
             for (int v = 0; v < 4; ++v)
-              s.gW2[(k0 + u) * TR_CPC + j0 + v] = (a[u][v] + alpha * s.W2[(k0 + u) * WS + c0 + j0 + v]) * invB;
+              s.gW2[(k0 + u) * TR_CPC + q4 + 4 * v] = (a[u][v] + alpha * s.W2[(k0 + u) * WS + c0 + q4 + 4 * v]) * invB;
         }
       }
-      if (tid < TR_CPC) {
-        float g = 0.0f;
-        for (int r = 0; r < B; ++r) g += s.h2T[tid * BM + r];
-        s.gb2[tid] = g * invB;
+      {  // gb2: warp w sums units w, w + 8
+        const int w = tid >> 5, ln = tid & 31;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          float g = 0.0f;
+          for (int r = ln; r < B; r += 32) g += s.h2T[(w + 8 * jj) * BM + r];
+          g = warp_sum(g);
+          if (ln == 0) s.gb2[w + 8 * jj] = g * invB;
+        }
       }
       __syncthreads();
       // own d2 units -> AT (the other CTAs finished reading our h1 units at (2))
@@ -334,17 +377,12 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
         const int o = (i / (B4 / 4)) * BM + (i % (B4 / 4)) * 4;
         *reinterpret_cast<float4*>(&s.AT[c0 * BM + o]) = ld4(&s.h2T[o]);
       }
+      mark(7);
       cluster.sync();  // (3) every CTA's d2 slice is written
-      for (int q = 1; q < C; ++q) {
-        const int rc = (c + q) % C;
-        const float* rA = cluster.map_shared_rank(s.AT, rc) + rc * TR_CPC * BM;
-        float* lA = s.AT + rc * TR_CPC * BM;
-        for (int i = tid; i < TR_CPC * (B4 / 4); i += TR_THREADS) {
-          const int o = (i / (B4 / 4)) * BM + (i % (B4 / 4)) * 4;
-          *reinterpret_cast<float4*>(&lA[o]) = ld4(&rA[o]);
-        }
-      }
+      mark(8);
+      gather(B4);  // the other CTAs' d2 units
       __syncthreads();
+      mark(9);
       // d1 = d2 W2^T . [h1 > 0] (own units, in place over h1T): W2 rows of the own units
       for (int tt = tid; tt < (B4 / 4) * (TR_CPC / 4); tt += TR_THREADS) {
         const int r0 = (tt / (TR_CPC / 4)) * 4, j0 = (tt % (TR_CPC / 4)) * 4;
@@ -382,12 +420,19 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
         }
         s.gW1[i] = (g + alpha * s.W1o[i]) * invB;
       }
-      if (tid < TR_CPC) {
-        float g = 0.0f;
-        for (int r = 0; r < B; ++r) g += s.h1T[tid * BM + r];
-        s.gb1[tid] = g * invB;
+      {  // gb1: warp w sums units w, w + 8
+        const int w = tid >> 5, ln = tid & 31;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          float g = 0.0f;
+          for (int r = ln; r < B; r += 32) g += s.h1T[(w + 8 * jj) * BM + r];
+          g = warp_sum(g);
+          if (ln == 0) s.gb1[w + 8 * jj] = g * invB;
+        }
       }
+      mark(10);
       cluster.sync();  // (4) every CTA is done reading W2 rows and our d2 slice
+      mark(11);
 
       // ---- Adam on the own parameters; new W2 columns -> every CTA's copy
       ++t;
@@ -395,13 +440,27 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
       b2t *= (double)p.beta2;
       const float lr_t = (float)((double)p.lr0 * sqrt(1.0 - b2t) / (1.0 - b1t));
       const float be1 = p.beta1, be2 = p.beta2, eps = p.eps;
-      for (int i = tid; i < H * TR_CPC; i += TR_THREADS) {
-        const int k = i / TR_CPC, j = i % TR_CPC;
-        float w = s.W2[k * WS + c0 + j], m = mW2[i], v = vW2[i];
-        adam(w, m, v, s.gW2[i], be1, be2, lr_t, eps);
-        mW2[i] = m;
-        vW2[i] = v;
-        for (int q = 0; q < C; ++q) cluster.map_shared_rank(s.W2, q)[k * WS + c0 + j] = w;
+      // W2 columns: four elements' moment loads in flight at a time
+      constexpr int NE = H * TR_CPC / TR_THREADS;  // 8 / 4 / 2 elements per thread
+      constexpr int NB = NE < 4 ? NE : 4;
+#pragma unroll 1
+      for (int e0 = 0; e0 < NE; e0 += NB) {
+        float mm[NB], vv[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          mm[u] = mW2[tid + (e0 + u) * TR_THREADS];
+          vv[u] = vW2[tid + (e0 + u) * TR_THREADS];
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int i = tid + (e0 + u) * TR_THREADS, k = i / TR_CPC, j = i % TR_CPC;
+          float w = s.W2[k * WS + c0 + j];
+          adam(w, mm[u], vv[u], s.gW2[i], be1, be2, lr_t, eps);
+          mW2[i] = mm[u];
+          vW2[i] = vv[u];
+#pragma unroll
+          for (int q = 0; q < C; ++q) cluster.map_shared_rank(s.W2, q)[k * WS + c0 + j] = w;
+        }
       }
       for (int i = tid; i < F * TR_CPC; i += TR_THREADS) adam(s.W1o[i], s.mW1[i], s.vW1[i], s.gW1[i], be1, be2, lr_t, eps);
       if (tid < TR_CPC) {
@@ -410,7 +469,9 @@ __global__ void __launch_bounds__(TR_THREADS, 1) train_kernel(const __grid_const
         adam(s.W3o[tid], s.mW3[tid], s.vW3[tid], s.gW3[tid], be1, be2, lr_t, eps);
       }
       if (tid == 0) adam(s.b3, s.mb3, s.vb3, s.gb3, be1, be2, lr_t, eps);  // identical on every CTA
+      mark(12);
       cluster.sync();  // (5) every W2 copy holds the new weights
+      mark(13);
     }
     // ---- epoch loss and the stopping rule (identical on every CTA of the member)
     const double el = acc / (double)p.n;
