@@ -1,18 +1,22 @@
-// K1, 16-bit variant (BF16, or FP16 with PREC = PREC_FP16) with three 128-row tiles in flight per SM (nets with at
-// most one hidden->hidden layer: 14-H-1 and 14-H-H-1, H <= 128).
+// K1, 16-bit variant (FP16 with PREC = PREC_FP16, or BF16) with NS = 4 128-row
+// tiles in flight per SM (nets with at most one hidden->hidden layer: 14-H-1
+// and 14-H-H-1, H <= 128).
 //
 // TMEM per slot is just the H-column accumulator region D:
-//   L1   : D[0, H)      = A0 (own 8-column area) x [W1; b1]          (N = H)
-//   epi1 : ReLU + bf16 pack of D[0, H) written IN PLACE to D[0, H/2): a thread
-//          reads chunk c (32 columns) before writing packed chunk c to columns
-//          16c .. 16c+15, which it has already read, so A1 needs no columns
+//   L1   : D[0, H)      = A0 x [W1; b1]                               (N = H)
+//   epi1 : ReLU + 16-bit pack of D[0, H) written IN PLACE to D[0, H/2): a
+//          thread reads chunk c (32 columns) before writing packed chunk c to
+//          columns 16c .. 16c+15, which it has already read, so A1 needs no columns
 //   L2a  : D[H/2, H)    = A1 x [W2; b2] (output neurons 0 .. H/2-1)     (N = H/2)
 //   fin-a: FP32 partial dot product over those neurons, then D[H/2, H) is free
 //   L2b  : D[H/2, H)    = A1 x [W2; b2] (output neurons H/2 .. H-1)
 //   fin-b: rest of the dot product, de-standardise, top-k
-// so 3 slots x H + 3 x 8 (A0) + 8 (ones block) columns fit in 512 (H = 128),
-// against 2 slots for the general kernel.  The next tile's A0 is decoded and
-// stored while L2b runs.
+// With NS = 4 the layer-1 operand A0 and the bias ones block live in shared
+// memory (SS-form UMMA for those two small steps), so 4 slots x H = all 512
+// columns at H = 128.  The next tile's A0 is decoded and stored while L2b runs.
+// The ENS instantiation (ensemble members >= 1) stages the member's fp32
+// accumulator slice of the tile into shared memory with a bulk copy issued
+// with the tile's L1.
 //
 // There is no central MMA warp: each slot's warpgroup issues its own UMMAs.
 // After the four warps finish writing (tcgen05.st) or reading (tcgen05.ld)
