@@ -53,13 +53,14 @@ def load_peaks():
     return 1590.0, 1400.0, "fallback"
 
 
-def ncu_traffic(workload, precision):
-    """Per-launch DRAM bytes of K1 from the committed ncu --set full summary."""
+def ncu_traffic(workload, precision, space=None):
+    """Per-launch DRAM bytes of K1 from the committed ncu --set full summary
+    (captures are keyed <space>/<precision>; a workload name is tried first)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(f"{workload}/{precision}")
+        e = d.get(f"{workload}/{precision}") or (d.get(f"{space}/{precision}") if space else None)
         return None if e is None else e.get("dram_bytes_per_launch")
     except Exception:
         return None
@@ -272,7 +273,8 @@ def main():
     ratio = PEAK_RATIO[mma_kind]
     dtype = DTYPE.get(precision, f"3x{'fp16' if mma_kind == 'f16' else 'tf32'} (fp32 path)")
     peak = burst * ratio
-    traffic = ncu_traffic(wl.name, precision)
+    # precision variants of a workload (cfg2_fp32, cfg2_bf16) share its captures
+    traffic = ncu_traffic(wl.name, precision, wl.space if wl.name.startswith(wl.space + "_") else None)
 
     # end to end through the public API: value table H2D + result D2H every step
     e2e = None
