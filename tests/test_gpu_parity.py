@@ -436,3 +436,47 @@ def test_cfg4_full_sweep_reevaluated_and_sampled(pk):
 def test_cfg2_full_sweep_sampled_property(pk):
     vl = workloads.space("cfg2")
     _full_sweep_checks(pk, workloads.load_model("cfg2_14-128-128-1"), vl, "fp16", 16, 2)
+
+
+# ------------------------------------------------------------------ scalers, device-feature encodings, NaN order
+@pytest.mark.parametrize("prec", ["fp16", "fp32"])
+def test_minmax_and_standard_scalers(pk, prec):
+    # the kernel implements the generic affine map z = (x - shift) / scale,
+    # so StandardScaler and min-max run through the same path
+    from oracle import scaler
+    vl = workloads.space("cfg2")
+    X = workloads.predict_rows(vl, 5000, seed=3)
+    for fit in (scaler.fit_standard, scaler.fit_minmax):
+        model = workloads.random_net(vl, [128, 128], seed=17)
+        model["x_shift"], model["x_scale"] = fit(X)
+        h = _handle(pk, model, prec)
+        b, n = 12_345_678, 150_001
+        t = h.eval_range(vl, b, b + n).cpu().numpy()
+        e = rel_err(t, osweep.times(model, vl, b, b + n), model["y_scale"])
+        assert e.max() <= TOL[prec], f"{fit.__name__} {prec}: {e.max():.3e}"
+
+
+def test_cfg4_gflops_encoding(pk):
+    # the device feature as DP GFLOPS instead of one-hot; a
+    # random 15-input ensemble whose constant feature is folded into b_1
+    vl = workloads.space("cfg2")
+    base = workloads.random_net(vl + [[513.0, 4700.0, 7500.0]], [128, 128], seed=19, ensemble=2)
+    model = workloads.with_device(base, workloads.device_features("gflops", "P100"))
+    assert model["widths"][0] == 15
+    h = _handle(pk, model, "fp16")
+    b, n = 50_000_001, 100_003
+    t = h.eval_range(vl, b, b + n).cpu().numpy()
+    assert rel_err(t, osweep.times(model, vl, b, b + n), model["y_scale"]).max() <= TOL["fp16"]
+
+
+def test_nan_predictions_rank_last_by_index(pk):
+    # NaN times order after +inf, ties by index: an all-NaN net's
+    # top-k is the first k indices of the range, times NaN
+    vl = workloads.space("cfg2")
+    model = workloads.all_ties_net(vl, [128, 128])
+    model["members"][0]["b"][-1][0] = float("nan")
+    for prec in ("fp16", "fp32"):
+        h = _handle(pk, model, prec)
+        idx, t, cnt = h.sweep(vl, 8, 777, 777 + 5000)
+        assert idx.cpu().tolist() == list(range(777, 785))
+        assert torch.isnan(t).all()
