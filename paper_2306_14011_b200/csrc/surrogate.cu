@@ -407,8 +407,11 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
   KParams& k = h->sp;
   std::vector<uint32_t> voff(P);
   for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
-  auto slot_val = [&](uint32_t slot, uint32_t d) -> double {  // StandardScaler / min-max affine map
-    if (slot < P) return (values[voff[slot] + d] - h->hshift[slot]) / h->hscale[slot];
+  // StandardScaler / min-max affine map z = (x - shift) / scale, evaluated as the
+  // kernels' explicit-batch prologue does: one fp32 FMA fma(fp32(x), fp32(1/scale),
+  // fp32(-shift/scale)) (|dz| ~ 1e-7 |z| against the exact map)
+  auto slot_val = [&](uint32_t slot, uint32_t d) -> double {
+    if (slot < P) return (double)std::fmaf((float)values[voff[slot] + d], h->mp.zinv[slot], h->mp.zc[slot]);
     return slot == P ? 1.0 : 0.0;
   };
   const uint32_t ng = K0 / spg;
@@ -973,8 +976,8 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   for (uint32_t e = 0; e < E; ++e) {
     mps[e].w_gmem = (const uint8_t*)h->d_w + e * wstride;
     for (uint32_t j = 0; j < (uint32_t)K0; ++j) {  // predict prologue constants (parameter bank)
-      mps[e].zsh[j] = j < P ? shift[j] : 0.0;
-      mps[e].zinv[j] = j < P ? 1.0 / scale[j] : 0.0;
+      mps[e].zinv[j] = j < P ? (float)(1.0 / scale[j]) : 0.0f;
+      mps[e].zc[j] = j < P ? (float)(-shift[j] / scale[j]) : 0.0f;
     }
   }
   h->members.swap(mps);

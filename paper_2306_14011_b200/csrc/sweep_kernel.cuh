@@ -71,8 +71,11 @@ struct KParams {
   // predict rows
   const float* x;
   uint32_t P;
-  double zsh[K0];            // predict prologue: z_j = (x_j - zsh_j) * zinv_j (double,
-  double zinv[K0];           // parameter bank; zinv = 1 / scale, P:273 StandardScaler)
+  // input map z_j = fma(x_j, zinv_j, zc_j), zinv = fp32(1 / scale), zc = fp32(-shift / scale)
+  // (P:273 StandardScaler); the host value table evaluates the same fp32 FMA, so a row
+  // predicted from HBM and the same config decoded in a sweep see identical operands
+  float zinv[K0];
+  float zc[K0];
   // model
   uint32_t NL;               // UMMA layers (= number of hidden layers)
   const void* w_gmem;
@@ -369,9 +372,9 @@ __device__ __forceinline__ void make_a0_row(const KParams& p, const float* xr, A
       if (j + 1 < (int)p.P) x1 = ld1(j + 1);
     }
     float z0 = 0.0f, z1 = 0.0f;
-    if (j < (int)p.P) z0 = __double2float_rn(((double)x0 - p.zsh[j]) * p.zinv[j]);
+    if (j < (int)p.P) z0 = fmaf(x0, p.zinv[j], p.zc[j]);
     else if (j == (int)p.P) z0 = 1.0f;
-    if (j + 1 < (int)p.P) z1 = __double2float_rn(((double)x1 - p.zsh[j + 1]) * p.zinv[j + 1]);
+    if (j + 1 < (int)p.P) z1 = fmaf(x1, p.zinv[j + 1], p.zc[j + 1]);
     else if (j + 1 == (int)p.P) z1 = 1.0f;
     if (is16(PREC)) {
       a.hi[j / 2] = pk16<PREC>(z0, z1);

@@ -23,13 +23,15 @@ ap.add_argument("--workload", default="cfg2")
 ap.add_argument("--rows", type=int, default=1 << 24)
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
+ap.add_argument("--precision", default=None)
 a = ap.parse_args()
 wl = workloads.WORKLOADS[a.workload]
 vl = workloads.space(wl.space)
 model = workloads.load_model(wl.weights)
 if wl.device_encoding:
     model = workloads.with_device(model, workloads.device_features(wl.device_encoding, wl.devices[-1]))
-h = pk.Surrogate(0).load(model, wl.precision)
+prec = a.precision or wl.precision
+h = pk.Surrogate(0).load(model, prec)
 # random configs of the space (raw values), generated on the host once: the rows a sampler would produce
 rng = np.random.default_rng(7)
 N = int(np.prod([len(v) for v in vl]))
@@ -74,11 +76,11 @@ k1_step = k1_ms / a.steps
 print(json.dumps({
     "metric": "surrogate_predict rows/s (explicit batch from HBM)", "value": a.rows / (ms / 1e3), "unit": "rows/s",
     "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-    "dtype": wl.precision, "data": "synthetic",
+    "dtype": prec, "data": "synthetic",
     "config": {"workload": wl.name, "rows": a.rows, "row_bytes_in": 4 * X.shape[1], "row_bytes_out": 4},
     "roofline": {"bound": "tensor", "achieved": flops / (k1_step / 1e3) / 1e12,
-                 "peak": burst * PEAK_RATIO[wl.precision], "unit": "TFLOP/s",
-                 "frac": flops / (k1_step / 1e3) / 1e12 / (burst * PEAK_RATIO[wl.precision]),
+                 "peak": burst * PEAK_RATIO[h.arith()[0]], "unit": "TFLOP/s",
+                 "frac": flops / (k1_step / 1e3) / 1e12 / (burst * PEAK_RATIO[h.arith()[0]]),
                  "hbm_GBps": a.rows * (4 * X.shape[1] + 4) / (k1_step / 1e3) / 1e9},
     "e2e": {"value": a.rows / (e2e_ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": int(X.nbytes),
             "d2h_bytes_per_step": int(4 * a.rows)}}))
