@@ -480,3 +480,38 @@ def test_nan_predictions_rank_last_by_index(pk):
         idx, t, cnt = h.sweep(vl, 8, 777, 777 + 5000)
         assert idx.cpu().tolist() == list(range(777, 785))
         assert torch.isnan(t).all()
+
+
+# ------------------------------------------------------------------ cfg2 full enumeration
+def _golden(name, k):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"{name}_full_top{k}_oracle.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated (scripts/make_golden_topk.py)")
+    return json.load(open(path))
+
+
+@pytest.mark.parametrize("prec,k", [("fp32", 16), ("fp32", 64), ("fp16", 16), ("fp16", 64), ("bf16", 16),
+                                    ("fp32_3xtf32", 16)])
+def test_cfg2_full_space_topk_vs_oracle_enumeration(pk, prec, k):
+    # the whole 15^7 space on the GPU against the oracle's float64 enumeration of
+    # every config (tests/golden/cfg2_full_top64_oracle.json, written by
+    # scripts/make_golden_topk.py from oracle/ only): G17 acceptance
+    g = _golden("cfg2", 64)
+    vl = workloads.space("cfg2")
+    model = workloads.load_model(g["weights"])
+    h = _handle(pk, model, prec)
+    idx, t, cnt = h.sweep(vl, k)
+    assert cnt == k
+    ri = np.array(g["idx"][:k], np.uint64)
+    rt = np.array(g["t"][:k])
+    check_topk(idx.cpu().numpy().astype(np.uint64), t.cpu().numpy(), ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
+    if prec.startswith("fp32"):
+        # the FP32 path's "exact top-k": the same set as the oracle unless oracle
+        # times tie within the tolerance at the k-th place
+        Tk = float(rt[-1])
+        gpu = set(idx.cpu().numpy().astype(np.uint64).tolist())
+        for i, ti in zip(ri.tolist(), rt.tolist()):
+            assert i in gpu or abs(ti - Tk) <= 2 * TOL[prec] * Tk
