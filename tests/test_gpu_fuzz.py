@@ -1,0 +1,67 @@
+"""Seeded randomized coverage of the kernel envelope against the oracle:
+parameter counts 1..15 (decoder groups with radix-1 and partially filled slots),
+radices 1..9, value lists with arbitrary spacing, 1-3 hidden layers of 32 / 64
+/ 128 units, every precision, k from 1 to 300, ranges that start mid-tile and
+end ragged.  A shape outside an envelope (e.g. an FP32-path net whose 3xTF32
+weights exceed shared memory) must be refused with SurrogateError, never run."""
+
+import numpy as np
+import pytest
+
+import workloads
+from oracle import space as ospace
+from oracle import sweep as osweep
+from tests.helpers import TOL, check_topk, need_gpu, rel_err
+
+pytestmark = pytest.mark.gpu
+
+PRECS = ["fp16", "bf16", "fp32", "tf32", "fp32_3xtf32"]
+
+
+def _case(seed):
+    rng = np.random.default_rng([seed, 0xF022])
+    P = int(rng.integers(1, 16))
+    radix = [int(r) for r in rng.integers(1, 10, P)]
+    while int(np.prod(radix)) > 3_000_000:
+        radix[int(rng.integers(0, P))] = max(1, radix[int(rng.integers(0, P))] // 2)
+    vl = [sorted(set((np.cumsum(rng.uniform(0.5, 50.0, r)) + rng.uniform(1, 100)).round(3).tolist()))
+          for r in radix]
+    vl = [v if len(v) == r else [1.0 + i for i in range(r)] for v, r in zip(vl, radix)]
+    H = int(rng.choice([32, 64, 128]))
+    hidden = [H] * int(rng.integers(1, 4))
+    prec = PRECS[seed % len(PRECS)]
+    return vl, hidden, prec, rng
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_envelope(seed):
+    pk = need_gpu()
+    vl, hidden, prec, rng = _case(seed)
+    model = workloads.random_net(vl, hidden, seed=seed + 100)
+    try:
+        h = pk.Surrogate(0).load(model, prec)
+    except pk.SurrogateError as e:
+        # UNSUPPORTED / RANGE only, and never for the 16-bit kernels (whole envelope)
+        assert ("status 7" in str(e) or "status 2" in str(e)) and prec not in ("fp16", "bf16"), e
+        return
+    N = ospace.cardinality([len(v) for v in vl])
+    b = int(rng.integers(0, max(1, N // 3)))
+    e = int(min(N, b + rng.integers(1, 300_000)))
+    try:
+        t = h.eval_range(vl, b, e).cpu().numpy()
+    except pk.SurrogateError as err:  # e.g. the FP16 range guard
+        assert "status 2" in str(err) or "status 7" in str(err), err
+        assert prec == "bf16" or False, f"{prec} refused a unit-scaled net: {err}"
+        return
+    ref = osweep.times(model, vl, b, e)
+    err = rel_err(t, ref, model["y_scale"])
+    assert err.max() <= TOL[prec], f"seed {seed} {prec} {hidden} P={len(vl)} [{b},{e}): {err.max():.3e}"
+    k = int(min(e - b, rng.integers(1, 300)))
+    idx, tk, cnt = h.sweep(vl, k, b, e)
+    assert cnt == k
+    ri, rt = osweep.topk(model, vl, k, b, e)
+    check_topk(idx.cpu().numpy()[:k].astype(np.uint64), tk.cpu().numpy()[:k], ri, rt,
+               lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
+    dec = h.decode_range(vl, b, min(e, b + 4096) - b).cpu().numpy().astype(np.int64)
+    assert np.array_equal(dec, ospace.decode(np.arange(b, min(e, b + 4096), dtype=np.uint64),
+                                             [len(v) for v in vl]))
