@@ -515,3 +515,17 @@ def test_cfg2_full_space_topk_vs_oracle_enumeration(pk, prec, k):
         gpu = set(idx.cpu().numpy().astype(np.uint64).tolist())
         for i, ti in zip(ri.tolist(), rt.tolist()):
             assert i in gpu or abs(ti - Tk) <= 2 * TOL[prec] * Tk
+
+
+def test_cfg4_full_space_topk_vs_oracle_enumeration(pk):
+    # the 8-member combined-GPU ensemble (17 inputs, one-hot V100) over the whole
+    # cfg2 space against the oracle's float64 enumeration (golden file)
+    g = _golden("cfg4", 16)
+    vl = workloads.space("cfg2")
+    model = workloads.with_device(workloads.load_model(g["weights"]),
+                                  workloads.device_features(g["device"][0], g["device"][1]))
+    for prec in ("fp16", "fp32"):
+        h = _handle(pk, model, prec)
+        idx, t, cnt = h.sweep(vl, 16)
+        check_topk(idx.cpu().numpy().astype(np.uint64), t.cpu().numpy(), np.array(g["idx"], np.uint64),
+                   np.array(g["t"]), lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
