@@ -881,6 +881,13 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     p.off_fin = (uint32_t)off;  // final-layer [w' (H floats), -b (H floats)] for shared-memory readers
     off += 2ull * H * 4;
     p.w_bytes = (uint32_t)align_up(std::max<size_t>(off, 128), 128);
+    {  // refuse at load time a net whose weight image cannot fit next to the smallest launch
+      KParams probe = p;
+      probe.P = P;
+      if (smem_layout(ki, probe, 0, 1, MODE_DENSE) > SMEM_MAX)
+        return fail(h, SURR_E_UNSUPPORTED, "weights of this net (%u B in the precision's operand format) do not fit "
+                    "shared memory", p.w_bytes);
+    }
     p.w_rank_stride = p.w_bytes;
     std::vector<uint8_t> img((size_t)p.w_bytes * ranks, 0);
 

@@ -41,18 +41,15 @@ def test_fuzz_envelope(seed):
     try:
         h = pk.Surrogate(0).load(model, prec)
     except pk.SurrogateError as e:
-        # UNSUPPORTED / RANGE only, and never for the 16-bit kernels (whole envelope)
-        assert ("status 7" in str(e) or "status 2" in str(e)) and prec not in ("fp16", "bf16"), e
+        # UNSUPPORTED only (e.g. 3xTF32 weights of a deep 128-wide net exceed shared
+        # memory: refused at load time), and never for the 16-bit kernels
+        assert "status 7" in str(e) and prec not in ("fp16", "bf16"), e
         return
     N = ospace.cardinality([len(v) for v in vl])
     b = int(rng.integers(0, max(1, N // 3)))
     e = int(min(N, b + rng.integers(1, 300_000)))
-    try:
-        t = h.eval_range(vl, b, e).cpu().numpy()
-    except pk.SurrogateError as err:  # e.g. the FP16 range guard
-        assert "status 2" in str(err) or "status 7" in str(err), err
-        assert prec == "bf16" or False, f"{prec} refused a unit-scaled net: {err}"
-        return
+    # a net the load accepted must run (unit-scaled inputs: no FP16 range refusal either)
+    t = h.eval_range(vl, b, e).cpu().numpy()
     ref = osweep.times(model, vl, b, e)
     err = rel_err(t, ref, model["y_scale"])
     assert err.max() <= TOL[prec], f"seed {seed} {prec} {hidden} P={len(vl)} [{b},{e}): {err.max():.3e}"
