@@ -1263,8 +1263,10 @@ surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, uint32_t E, 
       cudaMemset(dprof, 0, 16 * 8);
       tp.prof = dprof;
     }
-    const void* fn = H == 32 ? (const void*)&train_kernel<32> : H == 64 ? (const void*)&train_kernel<64>
-                                                                        : (const void*)&train_kernel<128>;
+    const bool push = E > 1;  // DSMEM push exchange for ensembles, pull for one member (measured)
+    const void* fn = H == 32  ? (push ? (const void*)&train_kernel<32, true> : (const void*)&train_kernel<32, false>)
+                     : H == 64 ? (push ? (const void*)&train_kernel<64, true> : (const void*)&train_kernel<64, false>)
+                               : (push ? (const void*)&train_kernel<128, true> : (const void*)&train_kernel<128, false>);
     const size_t smem = H == 32 ? sizeof(TrainSmem<32>) : H == 64 ? sizeof(TrainSmem<64>) : sizeof(TrainSmem<128>);
     if (smem > SMEM_MAX) { rc = fail(h, SURR_E_UNSUPPORTED, "training shared memory %zu B", smem); break; }
     TCU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
