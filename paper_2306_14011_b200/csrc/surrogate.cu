@@ -287,7 +287,7 @@ bool get_kernel(int prec, uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg 
       if (H == 128) { *ki = kinfo6<128>(); return true; }
     }
   }
-  if ((prec == PREC_FP32 || prec == PREC_FP32H) && NL <= 2) {
+  if (prec == PREC_FP32H || (prec == PREC_FP32 && NL <= 2)) {
 #define CASE5(P_, H_) \
   if (prec == P_ && H == H_) { *ki = kinfo5<P_, H_>(); return true; }
     CASE5(PREC_FP32, 32) CASE5(PREC_FP32, 64) CASE5(PREC_FP32, 128)
@@ -807,13 +807,13 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
     if (!m->W[l] || !m->b[l]) return fail(h, SURR_E_INVALID_ARG, "null layer %u", l);
   CU(cudaSetDevice(h->dev));
 
-  // the FP32 path runs as 3xFP16 where its kernel exists (H <= 128, <= 2 hidden
-  // layers: twice the tensor rate of 3xTF32, the same 22 significant bits),
-  // else (or when forced) as 3xTF32
+  // the FP32 path runs as 3xFP16 where its kernels exist (H <= 128: twice the
+  // tensor rate of 3xTF32, the same 22 significant bits), else (or when forced)
+  // as 3xTF32
   const int prec = m->precision == SURR_PREC_BF16   ? PREC_BF16
                    : m->precision == SURR_PREC_FP16 ? PREC_FP16
                    : m->precision == SURR_PREC_TF32 ? PREC_TF32
-                   : m->precision == SURR_PREC_FP32 && L - 1 <= 2 && H <= 128 ? PREC_FP32H
+                   : m->precision == SURR_PREC_FP32 && H <= 128 ? PREC_FP32H
                                                     : PREC_FP32;
   const uint32_t NL = L - 1;
   std::vector<double> shift(F), scale(F);

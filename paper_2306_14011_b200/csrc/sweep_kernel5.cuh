@@ -131,13 +131,18 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
           umma_f16_ss(dslot, d_a0l, d_b1, idesc, 1u);
           umma_f16_ss(dslot, d_a0h, d_b1lo, idesc, 1u);
         } else if (C::H16) {
-          const uint32_t d2 = dslot + C::Y_COL;
+          // layer l reads A (packed in place) from region (l - 1) & 1 and writes region
+          // l & 1 (D1 = region 0, Y = region 1): ping-pong for nets with > 1 hidden->hidden layer
+          const uint32_t d2 = dslot + (layer & 1) * H;
+          const uint32_t asrc = dslot + ((layer - 1) & 1) * H;
+          const uint64_t bh = d_b2 + (uint64_t)((((uint32_t)layer - 1) * p.stride_bh) >> 4);
+          const uint64_t bl = d_b2lo + (uint64_t)((((uint32_t)layer - 1) * p.stride_bh) >> 4);
 #pragma unroll
           for (int kk = 0; kk < H / 16; ++kk) {
-            const uint32_t ah = dslot + 32 * (kk >> 1) + 8 * (kk & 1);  // hi; lo at + 16
-            umma_f16_ts(d2, ah, d_b2 + kk * 16, idesc, kk > 0);
-            umma_f16_ts(d2, ah + 16, d_b2 + kk * 16, idesc, 1u);
-            umma_f16_ts(d2, ah, d_b2lo + kk * 16, idesc, 1u);
+            const uint32_t ah = asrc + 32 * (kk >> 1) + 8 * (kk & 1);  // hi; lo at + 16
+            umma_f16_ts(d2, ah, bh + kk * 16, idesc, kk > 0);
+            umma_f16_ts(d2, ah + 16, bh + kk * 16, idesc, 1u);
+            umma_f16_ts(d2, ah, bl + kk * 16, idesc, 1u);
           }
         } else if (layer == 0) {
 #pragma unroll
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
             }
           }
         }
-        umma_commit(&bars[(C::H16 && layer == 1) ? 6 + s : 4 + s]);
+        umma_commit(&bars[(C::H16 && layer == 1 && p.NL == 2) ? 6 + s : 4 + s]);
   };
   auto issue = [&](int layer) {
     tc_fence_before();
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
   };
   // separate Y region only with a hidden->hidden layer (14-H-1 nets: the final
   // layer reads D1, and the next L1 waits for those reads at the slot barrier)
-  const bool sep = C::SEP_Y && p.NL > 1;
+  const bool sep = C::SEP_Y && p.NL == 2;
   if (first && tile < p.num_tiles) {
     if (mode == MODE_PREDICT) make_a0_predict<PREC>(p, I < p.end ? I : p.begin, a0);
     else make_a0_sweep<PREC>(p, slut, D, a0);
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
     const bool has_next = tile + p.dTiles < p.num_tiles;
     float part = 0.0f;
     for (uint32_t l = 0; l < p.NL; ++l) {
-      if (C::H16 && l == 1) {
+      if (C::H16 && l == 1 && p.NL == 2) {
         mbar_wait(&bars[6 + s], phd2);
         phd2 ^= 1u;
       } else {
@@ -222,20 +227,28 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
 #pragma unroll
         for (int c = 0; C::H16 && c < C::CPS / 32; ++c) {
           // in place: chunk c (32 fp32 columns, read first) -> 16 hi + 16 lo fp16x2 columns
+          // of region l & 1; layers l >= 1 add their bias here (layer 1's rides in A0)
+          const uint32_t rcol = dcol + (l & 1u) * H;
           uint32_t v[32];
-          tmem_ld32(dcol + c * 32, v);
+          tmem_ld32(rcol + c * 32, v);
           tmem_wait_ld();
           uint32_t hv[16], lv[16];
+          const int col0 = (int)(q * C::CPS) + c * 32;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const float x0 = fmaxf(__uint_as_float(v[2 * j]), 0.0f), x1 = fmaxf(__uint_as_float(v[2 * j + 1]), 0.0f);
+            float y0 = __uint_as_float(v[2 * j]), y1 = __uint_as_float(v[2 * j + 1]);
+            if (l >= 1) {
+              y0 += p.hbias[(l - 1) & 1][col0 + 2 * j];
+              y1 += p.hbias[(l - 1) & 1][col0 + 2 * j + 1];
+            }
+            const float x0 = fmaxf(y0, 0.0f), x1 = fmaxf(y1, 0.0f);
             hv[j] = f16x2(x0, x1);
             float h0, h1;
             f16x2_to_f32(hv[j], h0, h1);
             lv[j] = f16x2(x0 - h0, x1 - h1);  // x - hi is exact in fp32; one rounding to fp16
           }
-          tmem_st16(dcol + c * 32, hv);
-          tmem_st16(dcol + c * 32 + 16, lv);
+          tmem_st16(rcol + c * 32, hv);
+          tmem_st16(rcol + c * 32 + 16, lv);
         }
 #pragma unroll
         for (int c = 0; !C::H16 && c < C::CPS / 32; ++c) {
@@ -254,7 +267,7 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
         }
         tmem_wait_st();
         if (tr) trace_ev(p, s, jr, 2);
-        issue(1);
+        issue((int)l + 1);  // the next layer (nets deeper than two layers: l + 1 > 1)
         if (C::H16 && sep && first && has_next) {
           // 3xFP16: L1 of this tile is done, so the next tile's A0 tiles (shared
           // memory) can be written now; sub 0's warps sync among themselves and
@@ -290,7 +303,8 @@ __global__ void __launch_bounds__(Cfg5<PREC, H>::THREADS, 1)
           }
           issue(0);
         }
-        const uint32_t fcol = dcol + (sep ? C::Y_COL : 0);
+        // the last layer's region: Y for the two-layer split, else by layer parity (3xFP16)
+        const uint32_t fcol = dcol + (C::H16 ? ((p.NL - 1) & 1u) * H : (sep ? C::Y_COL : 0));
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
         for (int c = 0; c < C::CPS / 32; ++c) {

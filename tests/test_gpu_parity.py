@@ -344,19 +344,26 @@ def test_cfg5_trained_slices_and_topk1024(pk, prec):
 
 
 def test_fp32_path_kernel_choice(pk):
-    # <= 2 hidden layers, H <= 128: 3xFP16 on kind::f16; deeper nets: 3xTF32
-    # (general kernel; its weights fit one SM up to H = 64 at 3 hidden layers)
+    # H <= 128: 3xFP16 on kind::f16 at any depth (deeper nets: ping-pong regions
+    # in the 2-slot kernel); 3xTF32 only when forced
     vl = workloads.space("cfg2")
     h = _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp32")
     assert h.arith()[:2] == ("f16", 3)
     assert _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp32_3xtf32").arith()[:2] == ("tf32", 3)
     assert _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp16").arith()[:2] == ("f16", 1)
-    deep = workloads.random_net(vl, [64, 64, 64], seed=5)
-    h = _handle(pk, deep, "fp32")
+    for hidden in ([64, 64, 64], [128, 128, 128], [32, 32, 32, 32]):
+        deep = workloads.random_net(vl, hidden, seed=5 + len(hidden))
+        h = _handle(pk, deep, "fp32")
+        assert h.arith()[:2] == ("f16", 3)
+        b, n = 100_000_003, 70_001
+        t = h.eval_range(vl, b, b + n).cpu().numpy()
+        assert rel_err(t, osweep.times(deep, vl, b, b + n), deep["y_scale"]).max() <= TOL["fp32"], hidden
+        idx, tk, cnt = h.sweep(vl, 16, b, b + n)
+        ri, rt = osweep.topk(deep, vl, 16, b, b + n)
+        check_topk(idx.cpu().numpy().astype(np.uint64), tk.cpu().numpy(), ri, rt,
+                   lambda i: osweep.times_at(deep, vl, i), TOL["fp32"], deep["y_scale"])
+    h = _handle(pk, workloads.random_net(vl, [64, 64, 64], seed=8), "fp32_3xtf32")
     assert h.arith()[:2] == ("tf32", 3)
-    b, n = 100_000_003, 70_001
-    t = h.eval_range(vl, b, b + n).cpu().numpy()
-    assert rel_err(t, osweep.times(deep, vl, b, b + n), deep["y_scale"]).max() <= TOL["fp32"]
     # issued tensor work of the cfg2 net: 16-bit L1 + (H + 16) x H bias-folded L2
     assert _handle(pk, workloads.load_model("cfg2_14-128-128-1"), "fp16").arith()[2] == 2 * (16 * 128 + 144 * 128)
 
