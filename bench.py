@@ -141,8 +141,9 @@ def run_reference(args, wl, rank):
            "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": wl.name, "space": f"{N} configs", "net": "-".join(map(str, model["widths"])),
-                      "k": wl.k, "precision": "fp64 (oracle)", "sample": f"{sample} consecutive configs per step"},
+           "config": {"workload": wl.name, "space": f"{wl.space}: {N} configs", "net": "-".join(map(str, model["widths"])),
+                      "k": wl.k, "precision": "fp64 (oracle)", "weights": f"oracle-trained ({wl.weights})",
+                      "sample": f"{sample} consecutive configs per step"},
            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
                             "sample": f"{sample} configs/step at offset |S|/3, numpy float64"},
            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
