@@ -354,28 +354,31 @@ __device__ __forceinline__ void make_a0_sweep4(const KParams& p, const uint8_t* 
 // table divides; the two agree to 1 ulp of double before the fp32 rounding),
 // slot P = 1 (bias), rest 0.  Column pairs are loaded (8-byte loads when P is
 // even) and converted one at a time to keep the live register set small.
-template <int PREC, bool SMEM = false>
-__device__ __forceinline__ void make_a0_row(const KParams& p, const float* xr, A0Regs& a) {
-  const bool even = (p.P & 1u) == 0;
+// PC >= 0: the parameter count as a compile-time constant (the paper's 14: no
+// per-slot compares); PC < 0: runtime p.P
+template <int PREC, bool SMEM, int PC>
+__device__ __forceinline__ void make_a0_row_n(const KParams& p, const float* xr, A0Regs& a) {
+  const int P = PC >= 0 ? PC : (int)p.P;
+  const bool even = (P & 1) == 0;
   // global rows: read-only path; staged rows: plain shared-memory loads
   auto ld2 = [&](int j) { return SMEM ? *reinterpret_cast<const float2*>(xr + j) : __ldg(reinterpret_cast<const float2*>(xr + j)); };
   auto ld1 = [&](int j) { return SMEM ? xr[j] : __ldg(xr + j); };
 #pragma unroll
   for (int j = 0; j < K0; j += 2) {
     float x0 = 0.0f, x1 = 0.0f;
-    if (j + 1 < (int)p.P && even) {
+    if (j + 1 < P && even) {
       const float2 v = ld2(j);
       x0 = v.x;
       x1 = v.y;
     } else {
-      if (j < (int)p.P) x0 = ld1(j);
-      if (j + 1 < (int)p.P) x1 = ld1(j + 1);
+      if (j < P) x0 = ld1(j);
+      if (j + 1 < P) x1 = ld1(j + 1);
     }
     float z0 = 0.0f, z1 = 0.0f;
-    if (j < (int)p.P) z0 = fmaf(x0, p.zinv[j], p.zc[j]);
-    else if (j == (int)p.P) z0 = 1.0f;
-    if (j + 1 < (int)p.P) z1 = fmaf(x1, p.zinv[j + 1], p.zc[j + 1]);
-    else if (j + 1 == (int)p.P) z1 = 1.0f;
+    if (j < P) z0 = fmaf(x0, p.zinv[j], p.zc[j]);
+    else if (j == P) z0 = 1.0f;
+    if (j + 1 < P) z1 = fmaf(x1, p.zinv[j + 1], p.zc[j + 1]);
+    else if (j + 1 == P) z1 = 1.0f;
     if (is16(PREC)) {
       a.hi[j / 2] = pk16<PREC>(z0, z1);
     } else if (PREC == PREC_FP32H) {  // fp16 hi + fp16(z - hi) lo
@@ -390,6 +393,11 @@ __device__ __forceinline__ void make_a0_row(const KParams& p, const float* xr, A
       a.lo[j + 1] = __float_as_uint(z1 - __uint_as_float(a.hi[j + 1]));
     }
   }
+}
+template <int PREC, bool SMEM = false>
+__device__ __forceinline__ void make_a0_row(const KParams& p, const float* xr, A0Regs& a) {
+  if (p.P == 14) make_a0_row_n<PREC, SMEM, 14>(p, xr, a);
+  else make_a0_row_n<PREC, SMEM, -1>(p, xr, a);
 }
 template <int PREC>
 __device__ __forceinline__ void make_a0_predict(const KParams& p, uint64_t r, A0Regs& a) {
