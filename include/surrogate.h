@@ -51,7 +51,8 @@ typedef enum {
  * de-standardisation always run in FP32 on CUDA cores. */
 typedef enum {
   SURR_PREC_BF16 = 0, /* BF16 operands, FP32 accumulate (tcgen05 kind::f16) */
-  SURR_PREC_FP32 = 1, /* "FP32 path": 3xTF32 split (hi*hi + hi*lo + lo*hi), kind::tf32 */
+  SURR_PREC_FP32 = 1, /* "FP32 path" (1e-5): 3xFP16 split hi*hi + lo*hi + hi*lo on kind::f16
+                         (hi = fp16(x), lo = fp16(x - hi): 22 significant bits), FP32 accumulate */
   SURR_PREC_TF32 = 2, /* 1xTF32 hidden layers, 3xTF32 first layer */
   SURR_PREC_FP16 = 3, /* IEEE FP16 operands, FP32 accumulate (kind::f16): BF16's tensor rate with
                          11 significant bits instead of 8 (activations must stay below 65504) */
@@ -86,7 +87,11 @@ typedef struct {
  * first-layer bias at load time.  Ensembles (E <= 64) run one fused pass per
  * member: members 0..E-2 accumulate t in an fp32 device buffer (chunks of
  * 2^28 configs), the last one averages and emits.  Kernel envelope:
- * H in {32, 64, 128}, 1 <= L-1 <= SURR_MAX_HIDDEN_LAYERS, P + 1 <= 16. */
+ * H in {32, 64, 128} (256: FP16 / BF16, CTA pairs), 1 <= L-1 <=
+ * SURR_MAX_HIDDEN_LAYERS, P + 1 <= 16; a net whose weight image in the
+ * precision's operand format does not fit shared memory is refused here
+ * (SURR_E_UNSUPPORTED).  FP16 operands add a per-space range check (any
+ * activation that can reach 65504 -> SURR_E_RANGE at the first sweep). */
 typedef struct {
   uint32_t num_layers;           /* L affine layers */
   const uint32_t *widths;        /* [L + 1] */
