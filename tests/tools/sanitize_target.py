@@ -45,6 +45,13 @@ def main():
         torch.cuda.synchronize()
         print(f"{name}: top-1 {int(idx[0])} {float(t[0]):.5f}, dense {float(dense.sum()):.3f}, "
               f"predict {float(tp.sum()):.3f}, merged {int(mi[0])}", flush=True)
+    # GPU training (one member: DSMEM pull exchange; two members: push exchange)
+    Xs, ys = workloads.training_rows(vl2, 420, seed=2)
+    for E in (1, 2):
+        inits = [workloads.glorot_init([14, 32, 32, 1], seed=10 + e) for e in range(E)]
+        perms = np.stack([workloads.epoch_permutations(420, 2, seed=20 + e) for e in range(E)])
+        res = pk.train_ensemble(inits, Xs, ys, perms, dict(max_epochs=2))
+        print(f"train E={E}: loss {res[0][2][-1]:.5f}", flush=True)
     print("sanitize_target done")
 
 
