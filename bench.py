@@ -164,8 +164,17 @@ def cpu_baseline(wl, model, vl, budget_s=12.0):
         done += chunk
     dt = time.perf_counter() - t0
     cores = max(i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()) or 1
+    # the same oracle on one host thread (T = nproc and T = 1)
+    with threadpoolctl.threadpool_limits(1):
+        d1, t1 = 0, time.perf_counter()
+        while time.perf_counter() - t1 < budget_s / 3:
+            osweep.topk(model, vl, wl.k, lo + d1, lo + d1 + (chunk >> 2), chunk=chunk >> 2)
+            d1 += chunk >> 2
+        dt1 = time.perf_counter() - t1
     return {"value": done / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
-            "sample": f"{done} consecutive configs of {wl.name} from |S|/2 ({dt:.1f} s, numpy float64 top-k)"}
+            "value_1thread": d1 / dt1,
+            "sample": f"{done} consecutive configs of {wl.name} from |S|/2 ({dt:.1f} s, numpy float64 top-k); "
+                      f"value_1thread: {d1} configs on one thread ({dt1:.1f} s)"}
 
 
 def main():
