@@ -536,3 +536,27 @@ def test_cfg4_full_space_topk_vs_oracle_enumeration(pk):
         idx, t, cnt = h.sweep(vl, 16)
         check_topk(idx.cpu().numpy().astype(np.uint64), t.cpu().numpy(), np.array(g["idx"], np.uint64),
                    np.array(g["t"]), lambda i: osweep.times_at(model, vl, i), TOL[prec], model["y_scale"])
+
+
+def test_non_default_stream_ordering(pk):
+    # the calls are stream-ordered on the caller's stream: the same results on a
+    # side stream (work queued behind a long kernel on that stream) as on the default one
+    vl = workloads.space("cfg2")
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, "fp16")
+    ref_i, ref_t, _ = h.sweep(vl, 16, 5_000_000, 9_000_000)
+    dense_ref = h.eval_range(vl, 1_000, 201_000)
+    X = torch.tensor(workloads.predict_rows(vl, 50_000, seed=4), dtype=torch.float32, device="cuda:0")
+    pred_ref = h.predict(X)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        busy = torch.randn(4096, 4096, device="cuda:0")
+        for _ in range(8):
+            busy = busy @ busy / 64.0  # keeps the side stream busy while the calls are queued
+        i2, t2, _ = h.sweep(vl, 16, 5_000_000, 9_000_000, stream=side)
+        d2 = h.eval_range(vl, 1_000, 201_000, stream=side)
+        p2 = h.predict(X, stream=side)
+    side.synchronize()
+    assert torch.equal(i2, ref_i) and torch.equal(t2, ref_t)
+    assert torch.equal(d2, dense_ref) and torch.equal(p2, pred_ref)
