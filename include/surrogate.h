@@ -135,7 +135,9 @@ surr_status surrogate_predict(surrogate_t *h, const float *x_dev, uint64_t n, fl
 /* Exhaustive sweep of [begin, end): the k smallest (t, I), sorted.
  * idx_dev[k], t_dev[k]; *count_host = min(k, end - begin).
  * k in 1..SURR_K_MAX.  The space's value lookup table is cached on the
- * handle and re-uploaded only when the descriptor changes. */
+ * handle and re-uploaded only when the descriptor changes; a change first
+ * waits for the work already queued on the device (sweeps queued earlier keep
+ * reading their own table), as does surrogate_load_weights. */
 surr_status surrogate_sweep(surrogate_t *h, const surr_space *space, uint32_t k, uint64_t *idx_dev, float *t_dev,
                             uint32_t *count_host, void *stream);
 

@@ -457,6 +457,9 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
       }
     }
   }
+  // sweeps queued earlier (on any stream) may still read the previous table:
+  // let them finish before it is replaced (a table change is rare; cached spaces skip this)
+  CU(cudaDeviceSynchronize());
   if (lut.size() > h->d_lut_cap) {
     if (h->d_lut) cudaFree(h->d_lut);
     h->d_lut = nullptr;
@@ -973,6 +976,7 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   std::vector<uint8_t> img(wstride * E);
   for (uint32_t e = 0; e < E; ++e) memcpy(img.data() + e * wstride, imgs[e].data(), wstride);
 
+  CU(cudaDeviceSynchronize());  // queued sweeps may still read the previous weights
   if (img.size() > h->d_w_cap) {
     cudaFree(h->d_w);
     h->d_w = nullptr;

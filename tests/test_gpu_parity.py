@@ -560,3 +560,25 @@ def test_non_default_stream_ordering(pk):
     side.synchronize()
     assert torch.equal(i2, ref_i) and torch.equal(t2, ref_t)
     assert torch.equal(d2, dense_ref) and torch.equal(p2, pred_ref)
+
+
+def test_space_change_while_sweeps_are_queued(pk):
+    # a sweep queued on a busy stream keeps its value table when the next call
+    # (same handle) switches to another space; the new weights of a reload do not
+    # leak into sweeps queued before it either
+    vl_a = workloads.space("cfg2")
+    vl_b = [list(np.asarray(v) * 2.0) for v in vl_a]  # same radices, other values
+    model = workloads.load_model("cfg2_14-128-128-1")
+    h = _handle(pk, model, "fp16")
+    ref_a = h.eval_range(vl_a, 0, 1 << 20).clone()
+    ref_b = h.eval_range(vl_b, 0, 1 << 20).clone()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        busy = torch.randn(4096, 4096, device="cuda:0")
+        for _ in range(8):
+            busy = busy @ busy / 64.0
+        ta = h.eval_range(vl_a, 0, 1 << 20, stream=side)
+        tb = h.eval_range(vl_b, 0, 1 << 20, stream=side)
+    side.synchronize()
+    assert torch.equal(ta, ref_a) and torch.equal(tb, ref_b)
