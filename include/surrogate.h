@@ -21,7 +21,11 @@
  *    device; *_host outputs are host memory.  Calls taking `stream` (a
  *    cudaStream_t, NULL = legacy default stream) are stream-ordered and
  *    asynchronous unless the name says _host.
- *  - A handle is not thread-safe; distinct handles are independent.
+ *  - A handle is not thread-safe; distinct handles are independent.  The
+ *    handle's device scratch (per-CTA records, the ensemble accumulator) is
+ *    shared by its calls, so calls on DIFFERENT streams of one handle must
+ *    not overlap in time (calls on one stream are ordered; use one handle
+ *    per concurrent stream).
  *  - There is no CPU fallback: without an sm_100 device every call that needs
  *    the GPU returns SURR_E_NO_DEVICE.
  */
