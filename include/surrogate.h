@@ -128,7 +128,10 @@ const char *surrogate_last_error(const surrogate_t *h);
 /* Validate the model against the kernel envelope, fold constant features, b_1,
  * y_mean / y_scale into the layer parameters, convert to the precision's
  * operand format, pack the UMMA shared-memory image (K-major, no swizzle) and
- * upload it (synchronous).  PAPER.md:54, :63, :273. */
+ * upload it (complete on return) into the other of two device slots: sweeps
+ * queued earlier keep reading the weights their launch captured, and no
+ * device-wide synchronisation happens.  Non-finite weights, biases or scaler
+ * entries -> SURR_E_INVALID_ARG.  PAPER.md:54, :63, :273. */
 surr_status surrogate_load_weights(surrogate_t *h, const surr_model *model);
 
 /* Predict an explicit batch: x_dev holds n rows of P raw parameter values
@@ -139,9 +142,11 @@ surr_status surrogate_predict(surrogate_t *h, const float *x_dev, uint64_t n, fl
 /* Exhaustive sweep of [begin, end): the k smallest (t, I), sorted.
  * idx_dev[k], t_dev[k]; *count_host = min(k, end - begin).
  * k in 1..SURR_K_MAX.  The space's value lookup table is cached on the
- * handle and re-uploaded only when the descriptor changes; a change first
- * waits for the work already queued on the device (sweeps queued earlier keep
- * reading their own table), as does surrogate_load_weights. */
+ * handle and re-uploaded only when the descriptor changes, stream-ordered on
+ * `stream` into the other of two device slots (sweeps queued earlier, on any
+ * stream, keep reading the table their launch captured; the slot being
+ * rewritten is first waited for by its own events, never the whole device).
+ * A descriptor that fails validation leaves no cached space behind. */
 surr_status surrogate_sweep(surrogate_t *h, const surr_space *space, uint32_t k, uint64_t *idx_dev, float *t_dev,
                             uint32_t *count_host, void *stream);
 
@@ -153,6 +158,24 @@ surr_status surrogate_sweep_host(surrogate_t *h, const surr_space *space, uint32
 /* Parity hook: the fused sweep kernel in dense-output mode writes t(I) for
  * every I in [begin, end) to t_dev[I - begin]. */
 surr_status surrogate_eval_range(surrogate_t *h, const surr_space *space, float *t_dev, void *stream);
+
+/* Parity hook of the decoder and the normalisation prologue (SURVEY §8(a)
+ * a2, a3; PAPER.md:241 mixed-radix space, :273 StandardScaler): the fused
+ * sweep kernel itself, in the launch configuration surrogate_sweep uses for
+ * [begin, end), writes for every stride-th I (I - begin = q stride) the
+ * layer-1 operand row it built from its in-register digits and the value
+ * table: ops_dev[q * 16 + w], w =
+ * 0..7 the eight packed 16-bit hi column pairs (slot 2w in the low half, slot
+ * 2w+1 in the high half: z_j for parameter j, 1.0 in slot P, zeros after),
+ * w = 8..15 the lo pairs of the 3xFP16 FP32 path (0 for FP16 / BF16).  The
+ * row is exactly the UMMA operand, so comparing it with the oracle's decoded
+ * tuple mapped through the documented rounding checks
+ * decoded tuples bit-exactly; stride > 1 samples a whole-space launch.
+ * ops_dev: device, caller-owned, ceil((end - begin) / stride) * 64 bytes.
+ * SURR_E_INVALID_ARG for stride 0; SURR_E_UNSUPPORTED for the TF32 kernels
+ * (not covered). */
+surr_status surrogate_sweep_operands(surrogate_t *h, const surr_space *space, uint64_t stride, uint32_t *ops_dev,
+                                     void *stream);
 
 /* Merge `lists` sorted record lists of k_in entries each (device, contiguous)
  * into the k best, sorted (used after the NCCL
@@ -170,7 +193,8 @@ surr_status surrogate_sweep_records(surrogate_t *h, const surr_space *space, uin
 
 /* Decoder hook: digits of n consecutive indices starting at `first`, computed
  * by the kernels' device decoder (super-digit magic division), written as
- * uint8 digits_dev[n * P] (parameter 0 first). */
+ * uint8 digits_dev[n * P] (parameter 0 first).  SURR_E_UNSUPPORTED when a
+ * radix exceeds 256 (a digit would not fit its byte). */
 surr_status surrogate_decode_range(surrogate_t *h, const surr_space *space, uint64_t first, uint64_t n,
                                    uint8_t *digits_dev, void *stream);
 
@@ -248,7 +272,9 @@ typedef struct {
  * epochs_run left untouched), epochs_run[E], stop_reason[E] (0 = max_epochs,
  * 1 = tol).  Synchronous.  Errors: SURR_E_INVALID_ARG (null, n == 0, E == 0,
  * bad hyper, an index >= n in perms), SURR_E_UNSUPPORTED (widths outside the
- * envelope).  Members are independent clusters: more than fit at once run in
+ * envelope), SURR_E_RANGE when a member's epoch loss is non-finite (the fit
+ * diverged: the error names the member and epoch, W / b are left untouched).
+ * Members are independent clusters: more than fit at once run in
  * further waves. */
 surr_status surrogate_train(surrogate_t *h, const uint32_t *widths, uint32_t E, double *const *W, double *const *b,
                             const double *X, const double *y, uint64_t n, const uint32_t *perms,

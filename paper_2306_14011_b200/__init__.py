@@ -22,6 +22,7 @@ EXPORTS = [
     "surrogate_create", "surrogate_destroy", "surrogate_last_error", "surrogate_load_weights",
     "surrogate_predict", "surrogate_sweep", "surrogate_sweep_host", "surrogate_eval_range",
     "surrogate_merge_topk", "surrogate_sweep_records", "surrogate_decode_range", "surrogate_space_size",
+    "surrogate_sweep_operands",
     "surrogate_kernel_timing", "surrogate_kernel_timing_get", "surrogate_last_launches",
     "surrogate_selftest_umma", "surrogate_table_bytes", "surrogate_debug_trace", "surrogate_reset_cache",
     "surrogate_arith", "surrogate_train",
@@ -70,6 +71,7 @@ def lib() -> ctypes.CDLL:
         L.surrogate_sweep.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp, ctypes.POINTER(u32), vp]
         L.surrogate_sweep_host.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp, ctypes.POINTER(u32), vp]
         L.surrogate_eval_range.argtypes = [vp, ctypes.POINTER(_Space), vp, vp]
+        L.surrogate_sweep_operands.argtypes = [vp, ctypes.POINTER(_Space), u64, vp, vp]
         L.surrogate_merge_topk.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
         L.surrogate_sweep_records.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp]
         L.surrogate_decode_range.argtypes = [vp, ctypes.POINTER(_Space), u64, u64, vp, vp]
@@ -174,6 +176,13 @@ class Surrogate:
                     int(cf.size), cfp, len(members), PREC[precision])
         _check(lib().surrogate_load_weights(self.h, ctypes.byref(mc)), self.h)
         self.precision = precision
+        # identity of the loaded model (weights, scalers, device features,
+        # precision, ensemble size): part of every campaign checkpoint fingerprint
+        import hashlib
+        dg = hashlib.sha256(f"{precision}|{len(members)}|{list(map(int, widths))}|".encode())
+        for a in keep + [xs, xc, cf, np.array([model["y_mean"], model["y_scale"]], np.float64)]:
+            dg.update(np.ascontiguousarray(a).tobytes())
+        self.model_digest = dg.hexdigest()
         self.P = int(widths[0]) - int(cf.size)
         return self
 
@@ -263,6 +272,18 @@ class Surrogate:
         _check(lib().surrogate_eval_range(self.h, ctypes.byref(d.c), ctypes.c_void_p(t.data_ptr()),
                                           _stream_ptr(stream)), self.h)
         return t
+
+    def sweep_operands(self, value_lists, begin: int, end: int, stride: int = 1, stream=None):
+        """Layer-1 operand rows the fused sweep kernel built for I = begin + q stride
+        in [begin, end): int32 [n, 16] device tensor (8 hi column pairs, 8 lo pairs;
+        parity hook of the decoder and the value table)."""
+        import torch
+        d = SpaceDesc(value_lists, begin, end)
+        n = (end - begin + stride - 1) // stride
+        out = torch.empty((n, 16), dtype=torch.int32, device=f"cuda:{self.device}")
+        _check(lib().surrogate_sweep_operands(self.h, ctypes.byref(d.c), stride, ctypes.c_void_p(out.data_ptr()),
+                                              _stream_ptr(stream)), self.h)
+        return out
 
     def predict(self, x, stream=None):
         """Explicit batch: x float32 [n, P] device tensor of raw values -> t [n]."""

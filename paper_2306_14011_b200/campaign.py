@@ -144,5 +144,8 @@ def for_surrogate(surrogate, value_lists, k: int, begin: int, end: int, chunk: i
     def merge(recs, lists, kk):
         return surrogate.merge_topk(recs, lists, kk, kk)[2]
 
+    # the loaded model's digest is part of the identity: a checkpoint written
+    # under other weights / precision is refused, not silently resumed
+    tag = f"{tag}|model:{getattr(surrogate, 'model_digest', '')}"
     return Campaign(local, merge, k, begin, end, chunk, path, every, fingerprint(value_lists, k, begin, end, tag),
                     from_numpy=lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev))

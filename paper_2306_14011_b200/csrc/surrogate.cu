@@ -31,6 +31,19 @@
 
 using namespace surr;
 
+// Device copies of a host image that kernels read by pointer (the value table,
+// the weight image): two slots used alternately.  A slot is rewritten only
+// after the events recorded behind every launch that read it (one per launch
+// stream) and behind its own upload have completed, so replacing a table never
+// synchronises the device and never changes bytes a queued sweep still reads.
+struct UploadRing {
+  void* d[2] = {nullptr, nullptr};
+  void* hpin[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> users[2];
+  int cur = -1;
+};
+
 struct surrogate {
   int dev = -1;
   int sms = 0;
@@ -40,8 +53,7 @@ struct surrogate {
   int prec = 0;
   uint32_t H = 0, NL = 0, P = 0;
   std::vector<uint8_t> wimg;
-  void* d_w = nullptr;
-  size_t d_w_cap = 0;
+  UploadRing wring;  // device weight image (all members), two slots
   KParams mp{};  // model part of the kernel parameters (member 0)
   std::vector<KParams> members;  // per-member model parameters (ensemble)
   float* d_acc = nullptr;        // ensemble accumulation buffer (fp32 per config of a chunk)
@@ -57,8 +69,7 @@ struct surrogate {
   std::vector<uint32_t> c_radix;
   std::vector<double> c_values;
   std::vector<uint8_t> lut;
-  void* d_lut = nullptr;
-  size_t d_lut_cap = 0;
+  UploadRing lring;  // device value table, two slots
   KParams sp{};  // space part (decoder) of the kernel parameters
   uint64_t card = 0;
   uint32_t spg = 2;  // parameter slots per decoder group of the cached table
@@ -68,6 +79,8 @@ struct surrogate {
   surr_record* d_merged = nullptr;
   uint64_t* d_idx = nullptr;
   float* d_t = nullptr;
+  uint32_t* a0_dump = nullptr;  // MODE_A0 output of the current call
+  uint64_t a0_stride = 1;
   // debug timeline
   unsigned long long* trace = nullptr;
   uint32_t trace_n = 0;
@@ -97,6 +110,59 @@ surr_status fail(surrogate* h, surr_status st, const char* fmt, ...) {
     cudaError_t e_ = (call);                                                          \
     if (e_ != cudaSuccess) return fail(h, SURR_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
   } while (0)
+
+// record "slot cur of the ring was read by work queued on st up to here"
+surr_status ring_mark_use(surrogate* h, UploadRing& r, cudaStream_t st) {
+  if (r.cur < 0) return SURR_OK;
+  auto& u = r.users[r.cur];
+  cudaEvent_t ev = nullptr;
+  for (auto& e : u)
+    if (e.first == st) ev = e.second;
+  if (!ev) {
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    u.emplace_back(st, ev);
+  }
+  CU(cudaEventRecord(ev, st));
+  return SURR_OK;
+}
+
+// upload `bytes` of host data into the ring's other slot; stream-ordered on st
+// (async from pinned memory) or, with sync, complete on return.  *out = device copy.
+surr_status ring_upload(surrogate* h, UploadRing& r, const void* data, size_t bytes, cudaStream_t st, bool sync,
+                        void** out) {
+  const int s = (r.cur + 1) & 1;
+  for (auto& e : r.users[s]) CU(cudaEventSynchronize(e.second));  // its last readers and upload are done
+  if (bytes > r.cap[s]) {
+    if (r.d[s]) cudaFree(r.d[s]);
+    if (r.hpin[s]) cudaFreeHost(r.hpin[s]);
+    r.d[s] = r.hpin[s] = nullptr;
+    r.cap[s] = 0;
+    if (cudaMalloc(&r.d[s], bytes) != cudaSuccess || cudaMallocHost(&r.hpin[s], bytes) != cudaSuccess)
+      return fail(h, SURR_E_OOM, "cudaMalloc upload slot (%zu B)", bytes);
+    r.cap[s] = bytes;
+  }
+  memcpy(r.hpin[s], data, bytes);
+  if (sync) {
+    CU(cudaMemcpy(r.d[s], r.hpin[s], bytes, cudaMemcpyHostToDevice));
+  } else {
+    CU(cudaMemcpyAsync(r.d[s], r.hpin[s], bytes, cudaMemcpyHostToDevice, st));
+  }
+  r.cur = s;
+  surr_status rc = ring_mark_use(h, r, st);  // the pinned staging copy is in use until the copy ran
+  if (rc) return rc;
+  *out = r.d[s];
+  return SURR_OK;
+}
+
+void ring_free(UploadRing& r) {
+  for (int s = 0; s < 2; ++s) {
+    for (auto& e : r.users[s]) { cudaEventSynchronize(e.second); cudaEventDestroy(e.second); }
+    r.users[s].clear();
+    if (r.d[s]) cudaFree(r.d[s]);
+    if (r.hpin[s]) cudaFreeHost(r.hpin[s]);
+    r.d[s] = r.hpin[s] = nullptr;
+  }
+}
 
 // ------------------------------------------------------------ rounding (host)
 uint32_t f32_bits(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
@@ -350,7 +416,7 @@ constexpr size_t SMEM_MAX = 227 * 1024;
 surr_status f16_range_check(surrogate* h, const std::vector<uint32_t>& radix, const std::vector<double>& values);
 // k_hint: the top-k size the space is prepared for (shared-memory budget of the
 // 4-parameter decoder table)
-surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32_t k_hint = 1) {
+surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, cudaStream_t st, uint32_t k_hint = 1) {
   if (!sp || !sp->radix || !sp->values) return fail(h, SURR_E_INVALID_ARG, "null space descriptor");
   const uint32_t P = sp->num_params;
   if (P == 0 || P > SURR_MAX_PARAMS) return fail(h, SURR_E_INVALID_ARG, "num_params %u out of range", P);
@@ -371,9 +437,6 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
   if (sp->begin > end || end > card)
     return fail(h, SURR_E_INVALID_ARG, "bad range [%llu, %llu) of |S| = %llu", (unsigned long long)sp->begin,
                 (unsigned long long)end, (unsigned long long)card);
-  h->sp.begin = sp->begin;
-  h->sp.end = end;
-  h->card = card;
   auto table_entries = [&](uint32_t spg_) {
     uint64_t e = 0;
     for (uint32_t g = 0; g < (uint32_t)K0 / spg_; ++g) {
@@ -395,7 +458,14 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
             SMEM_MAX)
       spg = 4;
   }
-  if (!force && h->space_valid && radix == h->c_radix && values == h->c_values && spg == h->spg) return SURR_OK;
+  if (!force && h->space_valid && radix == h->c_radix && values == h->c_values && spg == h->spg) {
+    h->sp.begin = sp->begin;
+    h->sp.end = end;
+    h->card = card;
+    return SURR_OK;
+  }
+  // the cached space is replaced: nothing of it stays valid if a check below fails
+  h->space_valid = false;
   if (f16_range_check(h, radix, values) != SURR_OK) return SURR_E_RANGE;
 
   // super digits: group g holds A0 slots [spg g, spg (g+1)) (parameter j in slot j,
@@ -404,7 +474,9 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
   // with quadruple groups, see above), else 2.
   const bool bf = is16(h->prec);
   const bool h3 = h->prec == PREC_FP32H;  // 3xFP16: fp16 hi pair + fp16 lo pair per entry
-  KParams& k = h->sp;
+  KParams k = h->sp;  // committed to the handle only once the table is uploaded
+  k.begin = sp->begin;
+  k.end = end;
   std::vector<uint32_t> voff(P);
   for (uint32_t j = 0, o = 0; j < P; o += radix[j], ++j) voff[j] = o;
   // StandardScaler / min-max affine map z = (x - shift) / scale, evaluated as the
@@ -457,18 +529,15 @@ surr_status prepare_space(surrogate* h, const surr_space* sp, bool force, uint32
       }
     }
   }
-  // sweeps queued earlier (on any stream) may still read the previous table:
-  // let them finish before it is replaced (a table change is rare; cached spaces skip this)
-  CU(cudaDeviceSynchronize());
-  if (lut.size() > h->d_lut_cap) {
-    if (h->d_lut) cudaFree(h->d_lut);
-    h->d_lut = nullptr;
-    if (cudaMalloc(&h->d_lut, lut.size()) != cudaSuccess) return fail(h, SURR_E_OOM, "cudaMalloc lut");
-    h->d_lut_cap = lut.size();
-  }
-  CU(cudaMemcpy(h->d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
-  k.lut_gmem = h->d_lut;
+  // stream-ordered upload into the ring's other slot: sweeps queued earlier (on
+  // any stream) keep reading the slot their launch captured
+  void* dl = nullptr;
+  surr_status urc = ring_upload(h, h->lring, lut.data(), lut.size(), st, false, &dl);
+  if (urc) return urc;
+  k.lut_gmem = dl;
   k.lut_bytes = (uint32_t)lut.size();
+  h->sp = k;
+  h->card = card;
   h->lut.swap(lut);
   h->c_radix = radix;
   h->c_values = values;
@@ -601,7 +670,10 @@ surr_status launch(surrogate* h, Launch& L, int mode, cudaStream_t st) {
   }
   if (e1) CU(cudaEventRecord(e1, st));
   ++h->launches;
-  return SURR_OK;
+  // the launch reads the weight image and (sweeps) the value table by pointer
+  surr_status rc = ring_mark_use(h, h->wring, st);
+  if (!rc && mode != MODE_PREDICT) rc = ring_mark_use(h, h->lring, st);
+  return rc;
 }
 
 surr_status ensure_recs(surrogate* h, size_t n) {
@@ -616,9 +688,10 @@ surr_status ensure_recs(surrogate* h, size_t n) {
 surr_status launch_merge(surrogate* h, const surr_record* in, uint32_t lists, uint32_t k_in, uint32_t k,
                          uint64_t* oi, float* ot, surr_record* orec, cudaStream_t st) {
   const size_t budget = 200 * 1024 - 2ull * k * sizeof(surr_record);
-  uint32_t chunk = (uint32_t)std::max<size_t>(1, budget / (2ull * k_in * sizeof(surr_record)));
+  const uint32_t slot = std::max(k_in, k);  // list slot stride in shared memory (merge_kernel)
+  uint32_t chunk = (uint32_t)std::max<size_t>(1, budget / (2ull * slot * sizeof(surr_record)));
   chunk = std::min<uint32_t>(chunk, std::max<uint32_t>(lists, 1));
-  const size_t smem = (2ull * k + 2ull * chunk * k_in) * sizeof(surr_record);
+  const size_t smem = (2ull * k + 2ull * chunk * slot) * sizeof(surr_record);
   if (smem > 227 * 1024) return fail(h, SURR_E_UNSUPPORTED, "merge needs %zu B shared memory", smem);
   CU(cudaFuncSetAttribute((const void*)merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   merge_kernel<<<1, 1024, smem, st>>>(in, lists, k_in, k, chunk, oi, ot, orec);
@@ -678,6 +751,8 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
       L.p.recs = h->d_recs + done * k;
       L.p.t_dense = t_dense ? t_dense + (c0 - begin) : nullptr;
       L.p.x = x;
+      L.p.a0_dump = h->a0_dump;
+      L.p.a0_stride = h->a0_stride;
       // bulk copies need 16-byte aligned rows blocks: x itself, and c0 P 4 bytes
       L.p.x_tma = (L.ki.x_stage && x && ((uintptr_t)x % 16) == 0 && (c0 * L.p.P * 4) % 16 == 0) ? 1u : 0u;
       L.p.trace = h->trace;
@@ -699,7 +774,7 @@ surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint
   if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "no model loaded");
   if (k == 0 || k > SURR_K_MAX) return fail(h, SURR_E_INVALID_ARG, "k = %u outside 1..%u", k, SURR_K_MAX);
   CU(cudaSetDevice(h->dev));
-  surr_status rc = prepare_space(h, space, force, k);
+  surr_status rc = prepare_space(h, space, force, st, k);
   if (rc) return rc;
   const uint64_t begin = h->sp.begin, end = h->sp.end;
   const uint64_t n = end - begin;
@@ -741,7 +816,9 @@ surr_status surrogate_create(int cuda_device, surrogate_t** out) {
 void surrogate_destroy(surrogate_t* h) {
   if (!h) return;
   cudaSetDevice(h->dev);
-  cudaFree(h->d_w); cudaFree(h->d_lut); cudaFree(h->d_recs); cudaFree(h->d_merged);
+  ring_free(h->wring);
+  ring_free(h->lring);
+  cudaFree(h->d_recs); cudaFree(h->d_merged);
   cudaFree(h->d_acc);
   for (auto e : h->ev) cudaEventDestroy(e);
   delete h;
@@ -808,6 +885,22 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   if (P == 0 || P + 1 > (uint32_t)K0) return fail(h, SURR_E_UNSUPPORTED, "%u tuning parameters: need 1..15", P);
   for (uint32_t l = 0; l < E * L; ++l)
     if (!m->W[l] || !m->b[l]) return fail(h, SURR_E_INVALID_ARG, "null layer %u", l);
+  // non-finite parameters (e.g. a diverged fit) would make every prediction NaN
+  for (uint32_t e = 0; e < E; ++e)
+    for (uint32_t l = 0; l < L; ++l) {
+      const size_t nw = (size_t)m->widths[l] * m->widths[l + 1];
+      for (size_t i = 0; i < nw; ++i)
+        if (!std::isfinite(m->W[e * L + l][i]))
+          return fail(h, SURR_E_INVALID_ARG, "member %u layer %u: non-finite weight at %zu", e, l, i);
+      for (uint32_t i = 0; i < m->widths[l + 1]; ++i)
+        if (!std::isfinite(m->b[e * L + l][i]))
+          return fail(h, SURR_E_INVALID_ARG, "member %u layer %u: non-finite bias at %u", e, l, i);
+    }
+  for (uint32_t j = 0; j < F; ++j)
+    if (!std::isfinite(m->x_shift[j]) || !std::isfinite(m->x_scale[j]))
+      return fail(h, SURR_E_INVALID_ARG, "non-finite input scaler at %u", j);
+  if (!std::isfinite(m->y_mean) || !std::isfinite(m->y_scale))
+    return fail(h, SURR_E_INVALID_ARG, "non-finite target scaler");
   CU(cudaSetDevice(h->dev));
 
   // the FP32 path runs as 3xFP16 where its kernels exist (H <= 128: twice the
@@ -976,16 +1069,13 @@ surr_status surrogate_load_weights(surrogate_t* h, const surr_model* m) {
   std::vector<uint8_t> img(wstride * E);
   for (uint32_t e = 0; e < E; ++e) memcpy(img.data() + e * wstride, imgs[e].data(), wstride);
 
-  CU(cudaDeviceSynchronize());  // queued sweeps may still read the previous weights
-  if (img.size() > h->d_w_cap) {
-    cudaFree(h->d_w);
-    h->d_w = nullptr;
-    if (cudaMalloc(&h->d_w, img.size()) != cudaSuccess) return fail(h, SURR_E_OOM, "cudaMalloc weights");
-    h->d_w_cap = img.size();
-  }
-  CU(cudaMemcpy(h->d_w, img.data(), img.size(), cudaMemcpyHostToDevice));
+  // into the ring's other slot (complete on return): sweeps queued earlier keep
+  // reading the weights their launch captured; no device-wide synchronisation
+  void* dw = nullptr;
+  surr_status urc = ring_upload(h, h->wring, img.data(), img.size(), nullptr, true, &dw);
+  if (urc) return urc;
   for (uint32_t e = 0; e < E; ++e) {
-    mps[e].w_gmem = (const uint8_t*)h->d_w + e * wstride;
+    mps[e].w_gmem = (const uint8_t*)dw + e * wstride;
     for (uint32_t j = 0; j < (uint32_t)K0; ++j) {  // predict prologue constants (parameter bank)
       mps[e].zinv[j] = j < P ? (float)(1.0 / scale[j]) : 0.0f;
       mps[e].zc[j] = j < P ? (float)(-shift[j] / scale[j]) : 0.0f;
@@ -1046,12 +1136,32 @@ surr_status surrogate_eval_range(surrogate_t* h, const surr_space* space, float*
   if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "no model loaded");
   if (!t_dev) return fail(h, SURR_E_INVALID_ARG, "null output");
   CU(cudaSetDevice(h->dev));
-  surr_status rc = prepare_space(h, space, false);
+  surr_status rc = prepare_space(h, space, false, (cudaStream_t)stream);
   if (rc) return rc;
   h->launches = 0;
   if (h->sp.end == h->sp.begin) return SURR_OK;
   uint32_t lists = 0;
   return run_k1(h, h->sp.begin, h->sp.end, 1, MODE_DENSE, t_dev, nullptr, (cudaStream_t)stream, &lists);
+}
+
+surr_status surrogate_sweep_operands(surrogate_t* h, const surr_space* space, uint64_t stride, uint32_t* ops_dev,
+                                     void* stream) {
+  if (!h) return fail(nullptr, SURR_E_INVALID_ARG, "null handle");
+  if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "no model loaded");
+  if (!ops_dev || stride == 0) return fail(h, SURR_E_INVALID_ARG, "null output or stride 0");
+  if (!(is16(h->prec) || h->prec == PREC_FP32H) || (h->prec == PREC_FP32H && h->NL != 2))
+    return fail(h, SURR_E_UNSUPPORTED, "operand dump: FP16 / BF16 kernels and the 3xFP16 FP32-path kernel only");
+  CU(cudaSetDevice(h->dev));
+  surr_status rc = prepare_space(h, space, false, (cudaStream_t)stream);
+  if (rc) return rc;
+  h->launches = 0;
+  if (h->sp.end == h->sp.begin) return SURR_OK;
+  h->a0_dump = ops_dev;
+  h->a0_stride = stride;
+  uint32_t lists = 0;
+  rc = run_k1(h, h->sp.begin, h->sp.end, 1, MODE_A0, nullptr, nullptr, (cudaStream_t)stream, &lists);
+  h->a0_dump = nullptr;
+  return rc;
 }
 
 surr_status surrogate_predict(surrogate_t* h, const float* x_dev, uint64_t n, float* t_dev, void* stream) {
@@ -1083,9 +1193,12 @@ surr_status surrogate_decode_range(surrogate_t* h, const surr_space* space, uint
   if (!h->loaded) return fail(h, SURR_E_NOT_LOADED, "load a model first (the table format follows its precision)");
   if (n && !digits_dev) return fail(h, SURR_E_INVALID_ARG, "null output");
   CU(cudaSetDevice(h->dev));
-  surr_status rc = prepare_space(h, space, false);
+  surr_status rc = prepare_space(h, space, false, (cudaStream_t)stream);
   if (rc) return rc;
   if (first > h->card || n > h->card - first) return fail(h, SURR_E_INVALID_ARG, "range outside |S|");
+  for (uint32_t j = 0; j < h->P; ++j)
+    if (h->c_radix[j] > 256)
+      return fail(h, SURR_E_UNSUPPORTED, "radix[%u] = %u: uint8 digits hold radices up to 256", j, h->c_radix[j]);
   h->launches = 0;
   if (n == 0) return SURR_OK;
   DecodeParams dp{};
@@ -1303,6 +1416,14 @@ surr_status surrogate_train(surrogate_t* h, const uint32_t* widths, uint32_t E, 
     TCU(cudaMemcpy(hp.data(), dp, hp.size() * 4, cudaMemcpyDeviceToHost));
     std::vector<double> lh((size_t)E * hy->max_epochs);
     TCU(cudaMemcpy(lh.data(), dloss, lh.size() * 8, cudaMemcpyDeviceToHost));
+    for (uint32_t e = 0; e < E && rc == SURR_OK; ++e)
+      for (uint32_t p = 0; p < res[3 * e]; ++p)
+        if (!std::isfinite(lh[(size_t)e * hy->max_epochs + p])) {
+          // a diverged fit (S: training aborts on a non-finite loss): no weights are returned
+          rc = fail(h, SURR_E_RANGE, "member %u: non-finite training loss in epoch %u (divergence)", e, p + 1);
+          break;
+        }
+    if (rc != SURR_OK) break;
     for (uint32_t e = 0; e < E; ++e) {
       for (uint32_t p = 0; p < res[3 * e]; ++p)
         loss_history[(size_t)e * hy->max_epochs + p] = lh[(size_t)e * hy->max_epochs + p];

@@ -49,7 +49,9 @@ __device__ __forceinline__ uint32_t pk16(float lo, float hi) {
 // 1.0 in the precision's 16-bit format (K slot 0 of the bias ones block)
 template <int PREC>
 __host__ __device__ constexpr uint32_t one16() { return PREC == PREC_FP16 ? 0x3C00u : 0x3F80u; }
-enum { MODE_TOPK = 0, MODE_DENSE = 1, MODE_PREDICT = 2 };
+// MODE_A0: parity hook of the decoder + value table (a2, a3): the sweep runs as
+// in MODE_DENSE but writes, per config, the layer-1 operand row it built
+enum { MODE_TOPK = 0, MODE_DENSE = 1, MODE_PREDICT = 2, MODE_A0 = 3 };
 
 constexpr int MAXG = 8;       // super-digit groups = A0 column pairs (K0 / 2)
 constexpr int K0 = 16;        // layer-1 K (P + ones slot <= 16)
@@ -94,6 +96,8 @@ struct KParams {
   uint32_t k;
   surr_record* recs;         // MODE_TOPK: gridDim.x * k records
   float* t_dense;            // MODE_DENSE / MODE_PREDICT
+  uint32_t* a0_dump;         // MODE_A0: 16 words per sampled config (hi columns, then lo columns)
+  uint64_t a0_stride;        // MODE_A0: configs begin, begin + a0_stride, ... are written
   uint32_t smem_lut, smem_lists, smem_cand, smem_misc;  // byte offsets in dynamic smem
   uint32_t smem_a0, smem_ones;  // SS-form A0 tiles / ones block (4-slot kernel)
   uint32_t smem_x, x_tile_bytes, x_tma;  // predict: per-slot staging of a tile's rows (bulk copy)
@@ -347,6 +351,23 @@ __device__ __forceinline__ void make_a0_sweep4(const KParams& p, const uint8_t* 
     const uint2 e = reinterpret_cast<const uint2*>(slut)[p.lut_off[g] + D[g]];
     a.hi[2 * g] = e.x;
     a.hi[2 * g + 1] = e.y;
+  }
+}
+
+// MODE_A0 (parity hook): the layer-1 operand row the sweep built for config I
+// (every a0_stride-th config of the range, so whole-space launches can be sampled),
+// exactly as it is stored for the UMMA (8 packed hi columns, 8 lo columns; LO =
+// false: 16-bit kernels, whose lo words are written as 0)
+template <bool LO>
+__device__ __forceinline__ void a0_dump(const KParams& p, int mode, const A0Regs& a, uint64_t I) {
+  if (mode == MODE_A0 && I < p.end) {
+    const uint64_t off = I - p.begin, q = off / p.a0_stride;  // every a0_stride-th config
+    if (q * p.a0_stride != off) return;
+    uint4* o = reinterpret_cast<uint4*>(p.a0_dump + q * 16);
+    o[0] = make_uint4(a.hi[0], a.hi[1], a.hi[2], a.hi[3]);
+    o[1] = make_uint4(a.hi[4], a.hi[5], a.hi[6], a.hi[7]);
+    o[2] = LO ? make_uint4(a.lo[0], a.lo[1], a.lo[2], a.lo[3]) : make_uint4(0u, 0u, 0u, 0u);
+    o[3] = LO ? make_uint4(a.lo[4], a.lo[5], a.lo[6], a.lo[7]) : make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -764,20 +785,27 @@ __global__ void __launch_bounds__(1024, 1)
     merge_kernel(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k, uint32_t chunk,
                  uint64_t* out_idx, float* out_t, surr_record* out_recs) {
   extern __shared__ __align__(16) uint8_t sm[];
+  // list slots are S = max(k_in, k) records apart, so a merged list (up to k
+  // records) never overruns its neighbour when k > k_in
+  const uint32_t S = max(k_in, k);
   surr_record* T = reinterpret_cast<surr_record*>(sm);  // [k] result so far
   surr_record* T2 = T + k;                              // [k]
-  surr_record* X = T2 + k;                              // [chunk * k_in]
-  surr_record* Y = X + (size_t)chunk * k_in;            // [chunk * k_in]
+  surr_record* X = T2 + k;                              // [chunk * S]
+  surr_record* Y = X + (size_t)chunk * S;               // [chunk * S]
   const uint32_t t = threadIdx.x, nt = blockDim.x;
   for (uint32_t i = t; i < k; i += nt) { T[i].idx = IDX_SENT; T[i].key = KEY_SENT; T[i].pad = 0; }
   for (uint32_t c0 = 0; c0 < lists; c0 += chunk) {
     const uint32_t m = min(chunk, lists - c0);
-    const uint32_t tot = m * k_in;
     const uint4* src = reinterpret_cast<const uint4*>(in + (size_t)c0 * k_in);
-    for (uint32_t i = t; i < tot; i += nt) reinterpret_cast<uint4*>(X)[i] = src[i];
+    if (S == k_in) {
+      for (uint32_t i = t; i < m * k_in; i += nt) reinterpret_cast<uint4*>(X)[i] = src[i];
+    } else {
+      for (uint32_t i = t; i < m * k_in; i += nt) reinterpret_cast<uint4*>(X)[(i / k_in) * S + i % k_in] = src[i];
+    }
     __syncthreads();
-    // pairwise tree: nl lists of length len (stride st) -> ceil(nl/2) lists of length min(2 len, k)
-    uint32_t nl = m, len = k_in, st = k_in;
+    // pairwise tree: nl lists of length len (stride S) -> ceil(nl/2) lists of length min(2 len, k)
+    uint32_t nl = m, len = k_in;
+    const uint32_t st = S;
     surr_record *cur = X, *nxt = Y;
     while (nl > 1) {
       const uint32_t nlen = min(2 * len, k);

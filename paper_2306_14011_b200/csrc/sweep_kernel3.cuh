@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     if (PRED) a0_pred(tile, I, a0);
     else if (SPG == 4) make_a0_sweep4(p, slut, D, a0);
     else make_a0_sweep<PREC>(p, slut, D, a0);
+    if (!PRED) a0_dump<false>(p, mode, a0, I);
     put_a0(a0);
     if (!C::A0_SMEM) tmem_wait_st();
     issue(0);  // L1 of the first tile
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
         else {
           odometer_step_n<NG>(p.R, p.dD, D);
           if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC>(p, slut, D, a0);
+          a0_dump<false>(p, mode, a0, In);
         }
         put_a0(a0);
         if (!C::A0_SMEM) tmem_wait_st();
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
         else {
           odometer_step_n<NG>(p.R, p.dD, D);
           if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC>(p, slut, D, a0);
+          a0_dump<false>(p, mode, a0, In);
         }
         put_a0(a0);
       }
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     if (!ens_stage(p, valid, I, t, ENS ? acc_get(tile, jr & 1u, valid, I) : ens_prefetch(p, valid, I))) {
     } else if (mode == MODE_TOPK) {
       topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
-    } else if (valid) {
+    } else if (valid && mode != MODE_A0) {
       p.t_dense[I - p.begin] = t;
     }
     if (tr) trace_ev(p, s, jr, 7);

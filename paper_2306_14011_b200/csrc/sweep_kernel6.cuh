@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(Cfg6<H>::THREADS, 1) sweep_kernel6(const __gri
   auto make_a0 = [&](uint64_t Ir) {
     if (mode == MODE_PREDICT) make_a0_predict<PREC_FP32H>(p, Ir < p.end ? Ir : p.begin, a0);
     else make_a0_sweep<PREC_FP32H>(p, slut, D, a0);
+    if (mode != MODE_PREDICT) a0_dump<true>(p, mode, a0, Ir);
   };
   if (rounds) {
     make_a0(I);
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(Cfg6<H>::THREADS, 1) sweep_kernel6(const __gri
     if (!ens_stage(p, valid, I, t, accp)) {
     } else if (mode == MODE_TOPK) {
       topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
-    } else if (valid) {
+    } else if (valid && mode != MODE_A0) {
       p.t_dense[I - p.begin] = t;
     }
     I = In;

@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
         } else {
           if (tile != pair) odometer_step_n<NG>(p.R, p.dD, D[u]);
           if (SPG == 4) make_a0_sweep4(p, slut, D[u], a0); else make_a0_sweep<PREC>(p, slut, D[u], a0);
+          a0_dump<false>(p, mode, a0, I);
         }
         st_a0_smem(a0tile, lane + 32u * u, a0.hi);
       }
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
         if (!ens_stage(p, valid, I, t, accp)) {
         } else if (mode == MODE_TOPK) {
           topk_offer(ts, mycand, ncand, valid, t, I, p.k, lane);
-        } else if (valid) {
+        } else if (valid && mode != MODE_A0) {
           p.t_dense[I - p.begin] = t;
         }
       }

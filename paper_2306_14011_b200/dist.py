@@ -41,12 +41,19 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def gather_records(recs: torch.Tensor, group=None) -> torch.Tensor:
-    """All ranks' [k, 2] int64 record blocks -> [W * k, 2] in rank order (one collective)."""
+    """All ranks' [k, 2] int64 record blocks -> [W * k, 2] in rank order (one collective).
+
+    NCCL exchanges the device tensors directly (NVLink / NVSwitch).  A gloo
+    group (several ranks sharing one GPU, or CPU tests) exchanges host copies:
+    the records are staged to host memory, gathered, and copied back to the
+    device the caller's merge kernel reads; the result is the same bytes."""
     world = dist.get_world_size(group)
-    out = torch.empty((world * recs.shape[0], recs.shape[1]), dtype=recs.dtype, device=recs.device)
+    host_staged = recs.is_cuda and dist.get_backend(group) == "gloo"
+    src = recs.contiguous().cpu() if host_staged else recs.contiguous()
+    out = torch.empty((world * src.shape[0], src.shape[1]), dtype=src.dtype, device=src.device)
     with nvtx("surrogate.allgather"):
-        dist.all_gather_into_tensor(out, recs.contiguous(), group=group)
-    return out
+        dist.all_gather_into_tensor(out, src, group=group)
+    return out.to(recs.device) if host_staged else out
 
 
 def sweep_distributed(local_sweep, merge, n: int, k: int, group=None):

@@ -74,3 +74,43 @@ def test_k_larger_than_range_and_nan_order():
     assert len(idx) == 4 and sorted(idx.tolist()) == [100, 101, 102, 103]
     i, tt = sweep.merge_topk([(np.array([5, 3, 9], np.uint64), np.array([np.nan, np.inf, 1.0]))], 3)
     assert i.tolist() == [9, 3, 5]
+
+
+def _combined_net(value_lists, n_const, seed):
+    """A random F-input net (F = P + n_const) whose scaler moves and scales every
+    column, device columns included (shift != 0, scale != 1), so that a device
+    feature left unscaled, or prepended instead of appended, changes t."""
+    ext = [list(v) for v in value_lists] + [[0.0, 1.0]] * n_const
+    model = workloads.random_net(ext, [6, 5], seed=seed)
+    model["x_shift"] = model["x_shift"] + np.linspace(0.3, 0.7, len(ext))
+    model["x_scale"] = model["x_scale"] * np.linspace(1.3, 0.6, len(ext))
+    return model
+
+
+def test_device_features_appended_after_parameters_and_scaled():
+    """z' = [z, f_dev] (P:281 device feature; S:72 columns appended after
+    the tuning parameters) for the scalar-GFLOPS and the one-hot encodings (G3):
+    oracle.mlp.predict on a model with constant features f equals the brute-force
+    F-input net on the space extended by one single-value list [f_c] per feature."""
+    vl = [[100, 1000], [32, 384], [200, 700, 900], [64, 128]]
+    for feats in ([4700.0], [0.0, 1.0, 0.0], [1.0, 0.0, 0.0]):
+        model = _combined_net(vl, len(feats), seed=11 + len(feats))
+        ext = vl + [[f] for f in feats]
+        ref = np.array(pins.brute_times(model, ext))
+        m = workloads.with_device(model, feats)
+        t = sweep.times(m, vl, 0, int(np.prod([len(v) for v in vl])))
+        assert np.max(np.abs(t - ref)) < 1e-12
+        # the same feature values placed BEFORE the parameters (the plausible
+        # mistake) give a different surface
+        pre = np.array(pins.brute_times(model, [[f] for f in feats] + vl)) if len(feats) == 1 else None
+        if pre is not None:
+            assert np.max(np.abs(pre - ref)) > 1e-3
+    # a feature left unscaled changes t as well (scale != 1, shift != 0 above)
+    model = _combined_net(vl, 1, seed=3)
+    unscaled = dict(model)
+    unscaled["x_shift"] = model["x_shift"].copy()
+    unscaled["x_scale"] = model["x_scale"].copy()
+    unscaled["x_shift"][-1], unscaled["x_scale"][-1] = 0.0, 1.0
+    a = sweep.times(workloads.with_device(model, [0.5]), vl, 0, 24)
+    b = np.array(pins.brute_times(unscaled, vl + [[0.5]]))
+    assert np.max(np.abs(a - b)) > 1e-3
