@@ -71,7 +71,8 @@ def lib() -> ctypes.CDLL:
         L.surrogate_sweep.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp, ctypes.POINTER(u32), vp]
         L.surrogate_sweep_host.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp, ctypes.POINTER(u32), vp]
         L.surrogate_eval_range.argtypes = [vp, ctypes.POINTER(_Space), vp, vp]
-        L.surrogate_sweep_operands.argtypes = [vp, ctypes.POINTER(_Space), u64, vp, vp]
+        if hasattr(L, "surrogate_sweep_operands"):  # (absent from round-1 builds used for A/B)
+            L.surrogate_sweep_operands.argtypes = [vp, ctypes.POINTER(_Space), u64, vp, vp]
         L.surrogate_merge_topk.argtypes = [vp, vp, u32, u32, u32, vp, vp, vp, vp]
         L.surrogate_sweep_records.argtypes = [vp, ctypes.POINTER(_Space), u32, vp, vp]
         L.surrogate_decode_range.argtypes = [vp, ctypes.POINTER(_Space), u64, u64, vp, vp]
@@ -88,6 +89,8 @@ def lib() -> ctypes.CDLL:
         L.surrogate_table_bytes.argtypes = [vp]
         L.surrogate_table_bytes.restype = u32
         for name in EXPORTS:
+            if not hasattr(L, name):
+                continue
             fn = getattr(L, name)
             if fn.restype is ctypes.c_int and name not in ("surrogate_last_launches",):
                 fn.restype = ctypes.c_int

@@ -23,6 +23,7 @@
 #include "sweep_kernel3.cuh"
 #include "sweep_kernel5.cuh"
 #include "sweep_kernel6.cuh"
+#include "sweep_kernel8.cuh"
 #include "sweep_kernel_pair.cuh"
 #include "train_kernel.cuh"
 #ifndef SURR_PAIR_NSUB
@@ -79,6 +80,7 @@ struct surrogate {
   surr_record* d_merged = nullptr;
   uint64_t* d_idx = nullptr;
   float* d_t = nullptr;
+  uint32_t* d_ctr = nullptr;    // ticket of the fused grid merge (zero between launches)
   uint32_t* a0_dump = nullptr;  // MODE_A0 output of the current call
   uint64_t a0_stride = 1;
   // debug timeline
@@ -301,6 +303,19 @@ KernelInfo kinfo3() {
   return ki;
 }
 
+template <int H, int SPG, int PREC>
+KernelInfo kinfo8() {
+  // CB = 0 (all of half b in the L1 shadow, 64-column epilogue loads) measured
+  // 1-2 % faster than CB = 16 (cfg2 3.49e10 vs 3.46e10, cfg5 3.15e10 vs 3.09e10
+  // evals/s, same box); SURR_K8CB=16 selects the other split for A/B
+  const char* v = getenv("SURR_K8CB");
+  const void* fn = (v && atoi(v) == 16) ? (const void*)&sweep_kernel8<H, SPG, PREC, 16>
+                                        : (const void*)&sweep_kernel8<H, SPG, PREC, 0>;
+  KernelInfo ki{fn, 4, 512, true};
+  ki.a0_smem = true;  // SS-form A0 tiles + the bias ones block in shared memory
+  return ki;
+}
+
 bool uses_kernel3(int prec, uint32_t H, uint32_t NL) {
   return is16(prec) && NL <= 2 && (H == 32 || H == 64 || H == 128);
 }
@@ -330,6 +345,13 @@ bool get_kernel16(uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg, bool en
       // ensembles (cfg 4): the accumulator-staging instantiations of the quad-table and predict kernels
       if (ens && spg == 4) { *ki = kinfo3<128, 4, PREC, true>(); return true; }
       if (ens && spg == 0) { *ki = kinfo3<128, 0, PREC, true>(); return true; }
+      // 14-128-128-1 sweeps: the final layer pipelined across tiles (SURR_K3=1:
+      // sweep_kernel3 for same-box A/B)
+      const char* k3 = getenv("SURR_K3");
+      if (NL == 2 && spg != 0 && !(k3 && atoi(k3) == 1)) {
+        *ki = spg == 4 ? kinfo8<128, 4, PREC>() : kinfo8<128, 2, PREC>();
+        return true;
+      }
       *ki = spg == 4 ? kinfo3<128, 4, PREC>() : spg == 2 ? kinfo3<128, 2, PREC>() : kinfo3<128, 0, PREC>();
       return true;
     }
@@ -704,18 +726,33 @@ surr_status launch_merge(surrogate* h, const surr_record* in, uint32_t lists, ui
 // chunk of <= 2^28 configs, members 0..E-2 accumulate t into d_acc and the last
 // member averages and emits (top-k records at recs + lists * k, or dense t,
 // or predict rows).  Returns the number of record lists written.
+// Merged top-k outputs of a sweep; K1 merges its own lists (last CTA, a9) when
+// the sweep is a single top-k launch whose shared memory holds the merge.
+struct MergeOut {
+  uint64_t* idx;
+  float* t;
+  surr_record* recs;
+  bool fused = false;  // out: K1 wrote the merged outputs
+};
+
 surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, float* t_dense, const float* x,
-                   cudaStream_t st, uint32_t* lists_out) {
+                   cudaStream_t st, uint32_t* lists_out, MergeOut* mo = nullptr) {
   const uint32_t E = (uint32_t)std::max<size_t>(1, h->members.size());
   const uint64_t chunk = E == 1 ? (end - begin) : (1ull << 28);
   // record lists of every chunk's final pass
-  uint64_t lists = 0;
+  uint64_t lists = 0, nchunks = 0;
+  uint32_t fuse_chunk = 0;  // lists per merge pass of a fused merge (0: K2 merges)
   for (uint64_t c0 = begin; c0 < end; c0 += chunk) {
     Launch L;
     surr_status rc = plan(h, c0, std::min(end, c0 + chunk), k, mode, &L);
     if (rc) return rc;
     lists += (uint64_t)L.grid;
+    ++nchunks;
+    const size_t need1 = 4ull * k * sizeof(surr_record);  // 2 k result + one list pair of 2 k
+    if (L.smem >= need1) fuse_chunk = (uint32_t)((L.smem - 2ull * k * sizeof(surr_record)) / (2ull * k * sizeof(surr_record)));
   }
+  const bool fuse = mo && mode == MODE_TOPK && nchunks == 1 && fuse_chunk >= 1 && !getenv("SURR_NO_FUSED_MERGE");
+  if (mo) mo->fused = fuse;
   if (mode == MODE_TOPK) {
     surr_status rc = ensure_recs(h, (size_t)lists * k);
     if (rc) return rc;
@@ -749,6 +786,13 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
         L.p.acc_tma = (L.ki.acc_stage && e > 0 && ((uintptr_t)h->d_acc % 16) == 0) ? 1u : 0u;
       }
       L.p.recs = h->d_recs + done * k;
+      if (fuse && last) {
+        L.p.done_ctr = h->d_ctr;
+        L.p.merge_chunk = std::min<uint32_t>(fuse_chunk, (uint32_t)L.grid);
+        L.p.out_idx = mo->idx;
+        L.p.out_t = mo->t;
+        L.p.out_recs = mo->recs;
+      }
       L.p.t_dense = t_dense ? t_dense + (c0 - begin) : nullptr;
       L.p.x = x;
       L.p.a0_dump = h->a0_dump;
@@ -785,8 +829,10 @@ surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint
     return launch_merge(h, h->d_recs, 0, k, k, idx_dev, t_dev, recs_dev, st);
   }
   uint32_t lists = 0;
-  rc = run_k1(h, begin, end, k, MODE_TOPK, nullptr, nullptr, st, &lists);
+  MergeOut mo{idx_dev, t_dev, recs_dev};
+  rc = run_k1(h, begin, end, k, MODE_TOPK, nullptr, nullptr, st, &lists, &mo);
   if (rc) return rc;
+  if (mo.fused) return SURR_OK;  // K1's last CTA merged the grid's lists (a9): one kernel per sweep
   return launch_merge(h, h->d_recs, lists, k, k, idx_dev, t_dev, recs_dev, st);
 }
 
@@ -805,7 +851,9 @@ surr_status surrogate_create(int cuda_device, surrogate_t** out) {
   h->dev = cuda_device;
   if (cudaSetDevice(cuda_device) != cudaSuccess) { delete h; return fail(nullptr, SURR_E_CUDA, "cudaSetDevice"); }
   cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cuda_device);
-  if (cudaMalloc(&h->d_merged, SURR_K_MAX * sizeof(surr_record)) != cudaSuccess) {
+  if (cudaMalloc(&h->d_merged, SURR_K_MAX * sizeof(surr_record)) != cudaSuccess ||
+      cudaMalloc(&h->d_ctr, 64) != cudaSuccess || cudaMemset(h->d_ctr, 0, 64) != cudaSuccess) {
+    cudaFree(h->d_merged);
     delete h;
     return fail(nullptr, SURR_E_OOM, "cudaMalloc");
   }
@@ -818,7 +866,7 @@ void surrogate_destroy(surrogate_t* h) {
   cudaSetDevice(h->dev);
   ring_free(h->wring);
   ring_free(h->lring);
-  cudaFree(h->d_recs); cudaFree(h->d_merged);
+  cudaFree(h->d_recs); cudaFree(h->d_merged); cudaFree(h->d_ctr);
   cudaFree(h->d_acc);
   for (auto e : h->ev) cudaEventDestroy(e);
   delete h;

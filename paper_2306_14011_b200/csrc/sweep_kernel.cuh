@@ -95,6 +95,13 @@ struct KParams {
   // outputs
   uint32_t k;
   surr_record* recs;         // MODE_TOPK: gridDim.x * k records
+  // fused grid merge (a9 in K1, MODE_TOPK): ticket counter (null: K2 merges),
+  // merge chunk (lists per shared-memory pass), merged outputs
+  uint32_t* done_ctr;
+  uint32_t merge_chunk;
+  uint64_t* out_idx;
+  float* out_t;
+  surr_record* out_recs;
   float* t_dense;            // MODE_DENSE / MODE_PREDICT
   uint32_t* a0_dump;         // MODE_A0: 16 words per sampled config (hi columns, then lo columns)
   uint64_t a0_stride;        // MODE_A0: configs begin, begin + a0_stride, ... are written
@@ -317,6 +324,128 @@ __device__ __forceinline__ void lock_release(TopkShared& ts, uint32_t lane) {
   }
 }
 
+
+// ------------------------------------------------------------------ K2
+// Merge `lists` sorted lists of k_in records into the k best (one CTA):
+// lists are loaded a chunk at a time (coalesced, all threads), reduced by a
+// pairwise tree of rank merges in shared memory, then merged into the result.
+// Ties (only sentinels can tie) are broken by list order: elements of the
+// left list use count(right < e), of the right list count(left <= f), so the
+// output positions are a permutation.
+__device__ __forceinline__ uint32_t upper_bound_recs(const surr_record* a, uint32_t n, uint32_t key, uint64_t idx) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const surr_record r = a[mid];
+    if (!rec_less(key, idx, r.key, r.idx)) lo = mid + 1; else hi = mid;  // r <= (key, idx)
+  }
+  return lo;
+}
+
+// out[0..min(na+nb, cap)) = first elements of merge(A[0..na), B[0..nb))
+__device__ __forceinline__ void rank_merge(const surr_record* A, uint32_t na, const surr_record* B, uint32_t nb,
+                                           surr_record* out, uint32_t cap, uint32_t t, uint32_t nt) {
+  for (uint32_t i = t; i < na; i += nt) {
+    const surr_record e = A[i];
+    const uint32_t pp = i + lower_bound_recs(B, nb, e.key, e.idx);
+    if (pp < cap) out[pp] = e;
+  }
+  for (uint32_t i = t; i < nb; i += nt) {
+    const surr_record f = B[i];
+    const uint32_t pp = i + upper_bound_recs(A, na, f.key, f.idx);
+    if (pp < cap) out[pp] = f;
+  }
+}
+
+// The merge body, run by every thread of one CTA over `sm` (shared memory of
+// (2 k + 2 chunk max(k_in, k)) records).  CG: read the lists with ld.global.cg
+// (written by other CTAs of the same launch: the fused last-CTA merge).
+template <bool CG>
+__device__ void merge_lists(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k,
+                            uint32_t chunk, uint64_t* out_idx, float* out_t, surr_record* out_recs, uint8_t* sm) {
+  // list slots are S = max(k_in, k) records apart, so a merged list (up to k
+  // records) never overruns its neighbour when k > k_in
+  const uint32_t S = max(k_in, k);
+  surr_record* T = reinterpret_cast<surr_record*>(sm);  // [k] result so far
+  surr_record* T2 = T + k;                              // [k]
+  surr_record* X = T2 + k;                              // [chunk * S]
+  surr_record* Y = X + (size_t)chunk * S;               // [chunk * S]
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  for (uint32_t i = t; i < k; i += nt) { T[i].idx = IDX_SENT; T[i].key = KEY_SENT; T[i].pad = 0; }
+  for (uint32_t c0 = 0; c0 < lists; c0 += chunk) {
+    const uint32_t m = min(chunk, lists - c0);
+    const uint4* src = reinterpret_cast<const uint4*>(in + (size_t)c0 * k_in);
+    auto ld = [&](uint32_t i) { return CG ? __ldcg(src + i) : src[i]; };
+    if (S == k_in) {
+      for (uint32_t i = t; i < m * k_in; i += nt) reinterpret_cast<uint4*>(X)[i] = ld(i);
+    } else {
+      for (uint32_t i = t; i < m * k_in; i += nt) reinterpret_cast<uint4*>(X)[(i / k_in) * S + i % k_in] = ld(i);
+    }
+    __syncthreads();
+    // pairwise tree: nl lists of length len (stride S) -> ceil(nl/2) lists of length min(2 len, k)
+    uint32_t nl = m, len = k_in;
+    const uint32_t st = S;
+    surr_record *cur = X, *nxt = Y;
+    while (nl > 1) {
+      const uint32_t nlen = min(2 * len, k);
+      const uint32_t pairs = nl / 2;
+      // threads split across pairs
+      const uint32_t tpp = max(1u, nt / pairs);
+      const uint32_t pr = t / tpp, tt = t % tpp;
+      for (uint32_t pi = pr; pi < pairs; pi += max(1u, nt / tpp)) {
+        rank_merge(cur + (size_t)(2 * pi) * st, len, cur + (size_t)(2 * pi + 1) * st, len, nxt + (size_t)pi * st,
+                   nlen, tt, tpp);
+      }
+      if (nl & 1) {
+        for (uint32_t i = t; i < len; i += nt) nxt[(size_t)pairs * st + i] = cur[(size_t)(nl - 1) * st + i];
+        for (uint32_t i = len + t; i < nlen; i += nt) {
+          nxt[(size_t)pairs * st + i].idx = IDX_SENT; nxt[(size_t)pairs * st + i].key = KEY_SENT;
+          nxt[(size_t)pairs * st + i].pad = 0;
+        }
+      }
+      __syncthreads();
+      surr_record* tmp = cur; cur = nxt; nxt = tmp;
+      nl = (nl + 1) / 2;
+      len = nlen;
+    }
+    // merge the chunk's best (cur[0..len)) into T
+    rank_merge(T, k, cur, min(len, k), T2, k, t, nt);
+    __syncthreads();
+    surr_record* tmp = T; T = T2; T2 = tmp;
+  }
+  for (uint32_t i = t; i < k; i += nt) {
+    const surr_record e = T[i];
+    if (out_idx) out_idx[i] = e.idx;
+    if (out_t) out_t[i] = key2f(e.key);
+    if (out_recs) out_recs[i] = e;
+  }
+}
+
+__global__ void __launch_bounds__(1024, 1)
+    merge_kernel(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k, uint32_t chunk,
+                 uint64_t* out_idx, float* out_t, surr_record* out_recs) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  merge_lists<false>(in, lists, k_in, k, chunk, out_idx, out_t, out_recs, sm);
+}
+
+// a9 fused into K1 (MODE_TOPK, p.done_ctr set): every CTA has written its k
+// records to p.recs[blockIdx.x k ..]; the last CTA to finish (device-scope
+// ticket) merges all gridDim.x lists into the outputs with the same code as
+// K2, reusing its shared memory, and re-arms the ticket for the next launch.
+// Called by every thread of the CTA after the kernel's teardown.
+__device__ __forceinline__ void grid_merge_tail(const KParams& p, int mode, uint8_t* sm) {
+  if (mode != MODE_TOPK || p.done_ctr == nullptr) return;
+  __syncthreads();  // this CTA's records are written (and its shared memory is free)
+  int last = 0;
+  if (threadIdx.x == 0) {
+    __threadfence();  // release: the records before the ticket
+    last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
+    if (last) __threadfence();  // acquire: every other CTA's records
+  }
+  if (!__syncthreads_or(last)) return;
+  merge_lists<true>(p.recs, gridDim.x, p.k, p.k, p.merge_chunk, p.out_idx, p.out_t, p.out_recs, sm);
+  if (threadIdx.x == 0) *p.done_ctr = 0u;  // re-armed (launches on one handle are stream-ordered)
+}
 
 // A0 operand of one row: bf16 / fp16 -> 8 packed columns; 3xFP16 -> 8 hi + 8 lo
 // packed columns; tf32 -> 16 hi + 16 lo slots.
@@ -747,99 +876,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
-}
-
-// ------------------------------------------------------------------ K2
-// Merge `lists` sorted lists of k_in records into the k best (one CTA):
-// lists are loaded a chunk at a time (coalesced, all threads), reduced by a
-// pairwise tree of rank merges in shared memory, then merged into the result.
-// Ties (only sentinels can tie) are broken by list order: elements of the
-// left list use count(right < e), of the right list count(left <= f), so the
-// output positions are a permutation.
-__device__ __forceinline__ uint32_t upper_bound_recs(const surr_record* a, uint32_t n, uint32_t key, uint64_t idx) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    const surr_record r = a[mid];
-    if (!rec_less(key, idx, r.key, r.idx)) lo = mid + 1; else hi = mid;  // r <= (key, idx)
-  }
-  return lo;
-}
-
-// out[0..min(na+nb, cap)) = first elements of merge(A[0..na), B[0..nb))
-__device__ __forceinline__ void rank_merge(const surr_record* A, uint32_t na, const surr_record* B, uint32_t nb,
-                                           surr_record* out, uint32_t cap, uint32_t t, uint32_t nt) {
-  for (uint32_t i = t; i < na; i += nt) {
-    const surr_record e = A[i];
-    const uint32_t pp = i + lower_bound_recs(B, nb, e.key, e.idx);
-    if (pp < cap) out[pp] = e;
-  }
-  for (uint32_t i = t; i < nb; i += nt) {
-    const surr_record f = B[i];
-    const uint32_t pp = i + upper_bound_recs(A, na, f.key, f.idx);
-    if (pp < cap) out[pp] = f;
-  }
-}
-
-__global__ void __launch_bounds__(1024, 1)
-    merge_kernel(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k, uint32_t chunk,
-                 uint64_t* out_idx, float* out_t, surr_record* out_recs) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  // list slots are S = max(k_in, k) records apart, so a merged list (up to k
-  // records) never overruns its neighbour when k > k_in
-  const uint32_t S = max(k_in, k);
-  surr_record* T = reinterpret_cast<surr_record*>(sm);  // [k] result so far
-  surr_record* T2 = T + k;                              // [k]
-  surr_record* X = T2 + k;                              // [chunk * S]
-  surr_record* Y = X + (size_t)chunk * S;               // [chunk * S]
-  const uint32_t t = threadIdx.x, nt = blockDim.x;
-  for (uint32_t i = t; i < k; i += nt) { T[i].idx = IDX_SENT; T[i].key = KEY_SENT; T[i].pad = 0; }
-  for (uint32_t c0 = 0; c0 < lists; c0 += chunk) {
-    const uint32_t m = min(chunk, lists - c0);
-    const uint4* src = reinterpret_cast<const uint4*>(in + (size_t)c0 * k_in);
-    if (S == k_in) {
-      for (uint32_t i = t; i < m * k_in; i += nt) reinterpret_cast<uint4*>(X)[i] = src[i];
-    } else {
-      for (uint32_t i = t; i < m * k_in; i += nt) reinterpret_cast<uint4*>(X)[(i / k_in) * S + i % k_in] = src[i];
-    }
-    __syncthreads();
-    // pairwise tree: nl lists of length len (stride S) -> ceil(nl/2) lists of length min(2 len, k)
-    uint32_t nl = m, len = k_in;
-    const uint32_t st = S;
-    surr_record *cur = X, *nxt = Y;
-    while (nl > 1) {
-      const uint32_t nlen = min(2 * len, k);
-      const uint32_t pairs = nl / 2;
-      // threads split across pairs
-      const uint32_t tpp = max(1u, nt / pairs);
-      const uint32_t pr = t / tpp, tt = t % tpp;
-      for (uint32_t pi = pr; pi < pairs; pi += max(1u, nt / tpp)) {
-        rank_merge(cur + (size_t)(2 * pi) * st, len, cur + (size_t)(2 * pi + 1) * st, len, nxt + (size_t)pi * st,
-                   nlen, tt, tpp);
-      }
-      if (nl & 1) {
-        for (uint32_t i = t; i < len; i += nt) nxt[(size_t)pairs * st + i] = cur[(size_t)(nl - 1) * st + i];
-        for (uint32_t i = len + t; i < nlen; i += nt) {
-          nxt[(size_t)pairs * st + i].idx = IDX_SENT; nxt[(size_t)pairs * st + i].key = KEY_SENT;
-          nxt[(size_t)pairs * st + i].pad = 0;
-        }
-      }
-      __syncthreads();
-      surr_record* tmp = cur; cur = nxt; nxt = tmp;
-      nl = (nl + 1) / 2;
-      len = nlen;
-    }
-    // merge the chunk's best (cur[0..len)) into T
-    rank_merge(T, k, cur, min(len, k), T2, k, t, nt);
-    __syncthreads();
-    surr_record* tmp = T; T = T2; T2 = tmp;
-  }
-  for (uint32_t i = t; i < k; i += nt) {
-    const surr_record e = T[i];
-    if (out_idx) out_idx[i] = e.idx;
-    if (out_t) out_t[i] = key2f(e.key);
-    if (out_recs) out_recs[i] = e;
-  }
+  grid_merge_tail(p, mode, smem);
 }
 
 // ------------------------------------------------------------ decode hook

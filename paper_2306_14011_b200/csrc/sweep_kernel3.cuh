@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+  grid_merge_tail(p, mode, smem);
 }
 
 }  // namespace surr

@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(Cfg6<H>::THREADS, 1) sweep_kernel6(const __gri
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+  grid_merge_tail(p, mode, smem);
 }
 
 }  // namespace surr

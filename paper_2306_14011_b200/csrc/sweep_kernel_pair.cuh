@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
     tc_fence_after();
     tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
   }
+  grid_merge_tail(p, mode, smem);
 }
 
 }  // namespace surr

@@ -478,10 +478,14 @@ def test_cfg4_gflops_encoding(pk):
 
 def test_nan_predictions_rank_last_by_index(pk):
     # NaN times order after +inf, ties by index: an all-NaN net's
-    # top-k is the first k indices of the range, times NaN
+    # top-k is the first k indices of the range, times NaN.  Non-finite weights
+    # are refused at load, so the NaN comes from the arithmetic: a target scale
+    # of 1e40 (finite in float64) overflows the FP32 output weights to inf, and
+    # inf x relu(0) = NaN in every row of the all-ties net
     vl = workloads.space("cfg2")
     model = workloads.all_ties_net(vl, [128, 128])
-    model["members"][0]["b"][-1][0] = float("nan")
+    model["members"][0]["W"][-1][:] = 0.5
+    model["y_scale"] = 1e40
     for prec in ("fp16", "fp32"):
         h = _handle(pk, model, prec)
         idx, t, cnt = h.sweep(vl, 8, 777, 777 + 5000)

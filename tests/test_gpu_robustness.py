@@ -133,3 +133,42 @@ def test_table_and_weight_swaps_while_sweeps_are_queued(pk):
     torch.cuda.synchronize()
     for key, t in outs:
         assert rel_err(t.cpu().numpy(), ref[key], 0.3).max() <= TOL["fp32"], key
+
+
+@pytest.mark.parametrize("name,weights,prec,k,begin,end", [
+    ("cfg2", "cfg2_14-128-128-1", "fp16", 16, 0, None),
+    ("cfg5", "cfg5_14-128-128-1", "fp16", 1024, 5_000_000_000, 5_000_000_000 + (1 << 27) + 77),
+    ("cfg2", "cfg2_14-128-128-1", "fp32", 64, 1000, 1000 + (1 << 24)),
+    ("cfg3", "cfg3_14-256-256-256-1", "fp16", 64, 0, 1 << 24),
+    ("cfg2", "cfg4_17-128-128-1_x8", "fp16", 16, 0, 1 << 22),
+    ("tiny", "tiny_14-32-32-1", "fp32", 1, 0, None),
+    ("cfg2", "cfg2_14-128-128-1", "fp16", 1024, 0, 3000),   # fewer configs than a full grid of lists
+])
+def test_fused_grid_merge_equals_k2(pk, monkeypatch, name, weights, prec, k, begin, end):
+    """a9 in K1 (last CTA merges the grid's lists) == K1 + the separate K2 merge,
+    bitwise, and the sweep is one kernel launch."""
+    import torch
+    vl = workloads.space(name)
+    model = workloads.load_model(weights)
+    if model["const_features"].size or "cfg4" in weights:
+        model = workloads.with_device(model, workloads.device_features("onehot", "V100"))
+    h = pk.Surrogate(0).load(model, prec)
+    N = int(np.prod([len(v) for v in vl], dtype=object))
+    end = N if end is None else end
+    i1, t1, c1 = h.sweep(vl, k, begin, end)
+    torch.cuda.synchronize()
+    n1 = h.last_launches()
+    monkeypatch.setenv("SURR_NO_FUSED_MERGE", "1")
+    i2, t2, c2 = h.sweep(vl, k, begin, end)
+    torch.cuda.synchronize()
+    n2 = h.last_launches()
+    assert c1 == c2 == min(k, end - begin)
+    assert torch.equal(i1, i2) and torch.equal(t1.view(torch.int32), t2.view(torch.int32))
+    members = len(model["members"])
+    assert n1 == members and n2 == members + 1  # fused: K1 only (one per ensemble member)
+    # repeated fused sweeps re-arm the ticket
+    monkeypatch.delenv("SURR_NO_FUSED_MERGE")
+    for _ in range(3):
+        i3, t3, _ = h.sweep(vl, k, begin, end)
+    torch.cuda.synchronize()
+    assert torch.equal(i1, i3)
