@@ -290,6 +290,20 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   }
 #endif
 }
+// Asynchronous 16-byte store into CTA `cta`'s shared memory at the offset of
+// `dst`, completing 16 transaction bytes on the mbarrier at the offset of `bar`
+// in that CTA (st.async: the complete_tx is a release at cluster scope, the
+// waiter acquires with mbar_wait_cluster)
+__device__ __forceinline__ void st_async_v4(const void* dst, float a, float b, float c, float d, uint64_t* bar,
+                                            uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 rd, rb;\n\tmapa.shared::cluster.u32 rd, %0, %6;\n\t"
+      "mapa.shared::cluster.u32 rb, %1, %6;\n\t"
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [rd], {%2, %3, %4, %5}, [rb];\n\t}" ::"r"(
+          smem_u32(dst)),
+      "r"(smem_u32(bar)), "f"(a), "f"(b), "f"(c), "f"(d), "r"(cta)
+      : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {  // one warp in each CTA of the pair
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),

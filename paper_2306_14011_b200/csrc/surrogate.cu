@@ -24,6 +24,7 @@
 #include "sweep_kernel5.cuh"
 #include "sweep_kernel6.cuh"
 #include "sweep_kernel8.cuh"
+#include "sweep_kernel8e.cuh"
 #include "sweep_kernel_pair.cuh"
 #include "train_kernel.cuh"
 #ifndef SURR_PAIR_NSUB
@@ -252,6 +253,9 @@ struct KernelInfo {
   bool x_stage = false;    // predict rows staged in shared memory by bulk copies
   uint32_t a0_tiles = 1;   // shared-memory A0 tiles per slot (3xFP16: hi + lo)
   bool acc_stage = false;  // ensemble accumulator prefetched per tile into shared memory by bulk copies
+  bool ens_pair = false;   // single-pass ensemble on CTA pairs (cluster of 2, 128-row tiles, members split)
+  uint32_t w_mult = 1;     // member images resident per CTA (weight region = w_mult x w_bytes)
+  uint32_t xch_bytes = 0;  // shared-memory exchange buffers (ensemble pairs)
 };
 
 template <int H, int SPG, int PREC>
@@ -314,6 +318,38 @@ KernelInfo kinfo8() {
   KernelInfo ki{fn, 4, 512, true};
   ki.a0_smem = true;  // SS-form A0 tiles + the bias ones block in shared memory
   return ki;
+}
+
+template <int H, int SPG, int PREC, int GM>
+KernelInfo kinfo8e() {
+  KernelInfo ki{(const void*)&sweep_kernel8e<H, SPG, PREC, GM>, 4, 512, true};
+  ki.a0_smem = true;
+  ki.ens_pair = true;
+  ki.w_mult = GM;
+  ki.xch_bytes = 4 * 2 * TILE_M * 16;  // [slot][2 buffers][128 rows] x float4
+  return ki;
+}
+
+// single-pass ensembles: 16-bit 14-128-128-1 members (device features folded),
+// E = 4 or 8 (2 or 4 member images per CTA of the pair) (SURR_NO_ENS_PAIR=1: the multi-pass
+// path, for A/B)
+template <int PREC>
+bool get_kernel_ens_pair16(uint32_t spg, uint32_t E, KernelInfo* ki) {
+#define ENS_CASE(GM_)                                                     \
+  if (E == 2 * GM_) {                                                     \
+    *ki = spg == 4 ? kinfo8e<128, 4, PREC, GM_>() : kinfo8e<128, 2, PREC, GM_>(); \
+    return true;                                                          \
+  }
+  ENS_CASE(2) ENS_CASE(4)
+#undef ENS_CASE
+  return false;
+}
+bool get_kernel_ens_pair(int prec, uint32_t H, uint32_t NL, uint32_t spg, uint32_t E, KernelInfo* ki) {
+  const char* v = getenv("SURR_NO_ENS_PAIR");
+  if ((v && atoi(v) == 1) || H != 128 || NL != 2 || (spg != 2 && spg != 4)) return false;
+  if (prec == PREC_FP16) return get_kernel_ens_pair16<PREC_FP16>(spg, E, ki);
+  if (prec == PREC_BF16) return get_kernel_ens_pair16<PREC_BF16>(spg, E, ki);
+  return false;
 }
 
 bool uses_kernel3(int prec, uint32_t H, uint32_t NL) {
@@ -408,7 +444,7 @@ surr_status check_device(surrogate* h, int dev) {
 // dynamic shared-memory layout of one K1 launch (offsets into p); returns bytes
 size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_t k, int mode) {
   const int nslot = ki.nslot;
-  size_t off = align_up(p.w_bytes, 128);
+  size_t off = align_up((size_t)p.w_bytes * ki.w_mult, 128);
   p.smem_lut = (uint32_t)off;
   off = align_up(off + (mode == MODE_PREDICT ? 0 : lut_bytes), 128);
   p.smem_lists = (uint32_t)off;
@@ -429,7 +465,7 @@ size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_
   off = align_up(off, 128);
   p.smem_x = (uint32_t)off;
   p.x_tile_bytes = TILE_M * p.P * 4;  // a multiple of 16 (bulk-copy granule)
-  off += (mode == MODE_PREDICT && ki.x_stage) ? (size_t)nslot * p.x_tile_bytes : 0;
+  off += (mode == MODE_PREDICT && ki.x_stage) ? (size_t)nslot * p.x_tile_bytes : ki.xch_bytes;
   return off;
 }
 constexpr size_t SMEM_MAX = 227 * 1024;
@@ -622,10 +658,19 @@ struct Launch {
   KParams p;
 };
 
-surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L, uint32_t member = 0) {
-  if (!get_kernel(h->prec, h->H, h->NL, &L->ki, mode == MODE_PREDICT ? 0 : h->spg, h->members.size() > 1))
+surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, Launch* L, uint32_t member = 0,
+                 const KernelInfo* force = nullptr) {
+  if (force) L->ki = *force;
+  else if (!get_kernel(h->prec, h->H, h->NL, &L->ki, mode == MODE_PREDICT ? 0 : h->spg, h->members.size() > 1))
     return fail(h, SURR_E_UNSUPPORTED, "no kernel for H=%u", h->H);
   KParams p = h->members.empty() ? h->mp : h->members[member];
+  if (L->ki.ens_pair) {  // all members in one launch: member 0's image is the base of all of them
+    const uint32_t E = (uint32_t)h->members.size();
+    p.ens_gm = L->ki.w_mult;
+    p.ens_e = E;
+    for (uint32_t e = 0; e < E && e < 16; ++e) p.ens_c[e] = h->members[e].c_out;
+    p.inv_e = 1.0f / (float)E;
+  }
   const KParams& s = h->sp;
   if (mode != MODE_PREDICT) {
     memcpy(p.R, s.R, sizeof p.R);
@@ -644,10 +689,12 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
   uint64_t want = (p.num_tiles + nslot - 1) / nslot;
   if (L->ki.pair) {  // clusters of two CTAs, one 256-row tile per pair at a time
     L->grid = 2 * (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms / 2, p.num_tiles));
+  } else if (L->ki.ens_pair) {  // clusters of two CTAs sweeping the same tiles (members split)
+    L->grid = 2 * (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms / 2, want));
   } else {
     L->grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)h->sms, want));
   }
-  p.dTiles = (uint32_t)(nslot * L->grid);
+  p.dTiles = (uint32_t)(nslot * (L->ki.ens_pair ? L->grid / 2 : L->grid));
   if (mode != MODE_PREDICT) stride_digits(p.R, (uint64_t)p.dTiles * TILE_M, p.dD);
   p.k = mode == MODE_TOPK ? k : 1;
   L->smem = smem_layout(L->ki, p, p.lut_bytes, k, mode);
@@ -673,7 +720,7 @@ surr_status launch(surrogate* h, Launch& L, int mode, cudaStream_t st) {
     CU(cudaEventRecord(e0, st));
   }
   void* args[] = {(void*)&L.p, (void*)&mode};
-  if (L.ki.pair) {
+  if (L.ki.pair || L.ki.ens_pair) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(L.grid);
     cfg.blockDim = dim3(L.ki.threads);
@@ -738,6 +785,40 @@ struct MergeOut {
 surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mode, float* t_dense, const float* x,
                    cudaStream_t st, uint32_t* lists_out, MergeOut* mo = nullptr) {
   const uint32_t E = (uint32_t)std::max<size_t>(1, h->members.size());
+  // ensembles: one pass on CTA pairs when the members fit (no accumulator, one launch)
+  if (E > 1 && mode != MODE_PREDICT) {
+    KernelInfo kp;
+    Launch L;
+    if (get_kernel_ens_pair(h->prec, h->H, h->NL, h->spg, E, &kp) &&
+        plan(h, begin, end, k, mode, &L, 0, &kp) == SURR_OK) {
+      if (mode == MODE_TOPK) {
+        surr_status rc = ensure_recs(h, (size_t)L.grid * k);
+        if (rc) return rc;
+      }
+      L.p.recs = h->d_recs;
+      L.p.t_dense = t_dense;
+      L.p.a0_dump = h->a0_dump;
+      L.p.a0_stride = h->a0_stride;
+      L.p.trace = h->trace;
+      L.p.trace_n = h->trace_n;
+      const size_t need1 = 4ull * k * sizeof(surr_record);
+      const bool fuse = mo && mode == MODE_TOPK && L.smem >= need1 && !getenv("SURR_NO_FUSED_MERGE");
+      if (fuse) {
+        L.p.done_ctr = h->d_ctr;
+        L.p.merge_chunk = std::min<uint32_t>(
+            (uint32_t)((L.smem - 2ull * k * sizeof(surr_record)) / (2ull * k * sizeof(surr_record))), (uint32_t)L.grid);
+        L.p.out_idx = mo->idx;
+        L.p.out_t = mo->t;
+        L.p.out_recs = mo->recs;
+      }
+      if (mo) mo->fused = fuse;
+      surr_status rc = launch(h, L, mode, st);
+      if (rc) return rc;
+      *lists_out = (uint32_t)L.grid;
+      return SURR_OK;
+    }
+    h->err.clear();  // not applicable (shape, E, or shared memory): the multi-pass path below
+  }
   const uint64_t chunk = E == 1 ? (end - begin) : (1ull << 28);
   // record lists of every chunk's final pass
   uint64_t lists = 0, nchunks = 0;

@@ -115,6 +115,10 @@ struct KParams {
   uint32_t acc_mode;
   float inv_e;
   uint32_t smem_acc, acc_tma;  // 4-slot kernel: per-slot double buffer of a tile's t_acc (bulk copies)
+  // single-pass ensemble on CTA pairs (sweep_kernel8e): members per CTA, E,
+  // each member's de-standardisation constant, shared-memory weight region
+  uint32_t ens_gm, ens_e;
+  float ens_c[16];
   // debug timeline (CTA 0 only): trace[ev] = clock64 of event ev, or null
   unsigned long long* trace;
   uint32_t trace_n;

@@ -15,7 +15,10 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 prec = sys.argv[2] if len(sys.argv) > 2 else "bf16"
 wl = workloads.WORKLOADS[name]
 vl = workloads.space(wl.space)
-h = pk.Surrogate(0).load(workloads.load_model(wl.weights), prec)
+model = workloads.load_model(wl.weights)
+if wl.device_encoding:  # combined-training model: one target device (G3)
+    model = workloads.with_device(model, workloads.device_features(wl.device_encoding, wl.devices[-1]))
+h = pk.Surrogate(0).load(model, prec)
 for _ in range(2):
     idx, t, _ = h.sweep(vl, wl.k)
 torch.cuda.synchronize()

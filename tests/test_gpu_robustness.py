@@ -165,10 +165,52 @@ def test_fused_grid_merge_equals_k2(pk, monkeypatch, name, weights, prec, k, beg
     assert c1 == c2 == min(k, end - begin)
     assert torch.equal(i1, i2) and torch.equal(t1.view(torch.int32), t2.view(torch.int32))
     members = len(model["members"])
-    assert n1 == members and n2 == members + 1  # fused: K1 only (one per ensemble member)
+    if members == 8:  # the single-pass ensemble (CTA pairs): one launch either way
+        assert n1 == 1 and n2 == 2
+    else:
+        assert n1 == members and n2 == members + 1  # fused: K1 only
     # repeated fused sweeps re-arm the ticket
     monkeypatch.delenv("SURR_NO_FUSED_MERGE")
     for _ in range(3):
         i3, t3, _ = h.sweep(vl, k, begin, end)
     torch.cuda.synchronize()
     assert torch.equal(i1, i3)
+
+
+@pytest.mark.parametrize("members,prec,begin,n", [(8, "fp16", 0, None), (8, "bf16", 77_777_777, (1 << 20) + 13),
+                                                  (4, "fp16", 170859375 - 300_001, 300_001),
+                                                  (8, "fp16", 5, 1000)])
+def test_single_pass_ensemble_equals_multipass(pk, monkeypatch, members, prec, begin, n):
+    """the E-member ensemble in one pass on CTA pairs (members
+    split, per-row predictions exchanged through distributed shared memory, no
+    HBM accumulator) is bitwise the multi-pass path (one K1 pass per member with
+    an fp32 accumulator, members summed in order e = 0 .. E-1), dense times and
+    top-k, in one kernel launch per sweep."""
+    import torch
+    vl = workloads.space("cfg2")
+    if members == 8:
+        model = workloads.with_device(workloads.load_model("cfg4_17-128-128-1_x8"),
+                                      workloads.device_features("onehot", "P100"))
+    else:
+        model = workloads.random_net(vl, [128, 128], seed=31, ensemble=members)
+    h = pk.Surrogate(0).load(model, prec)
+    N = 170859375
+    end = N if n is None else begin + n
+    k = 16
+    i1, t1, _ = h.sweep(vl, k, begin, end)
+    torch.cuda.synchronize()
+    assert h.last_launches() == 1
+    d1 = h.eval_range(vl, begin, min(end, begin + (1 << 20)))
+    torch.cuda.synchronize()
+    monkeypatch.setenv("SURR_NO_ENS_PAIR", "1")
+    i2, t2, _ = h.sweep(vl, k, begin, end)
+    torch.cuda.synchronize()
+    assert h.last_launches() == members  # multi-pass: one K1 per member (merge fused into the last)
+    d2 = h.eval_range(vl, begin, min(end, begin + (1 << 20)))
+    torch.cuda.synchronize()
+    assert torch.equal(d1.view(torch.int32), d2.view(torch.int32)), \
+        f"{int((d1 != d2).sum())} rows differ between the single-pass and the multi-pass ensemble"
+    assert torch.equal(i1, i2) and torch.equal(t1.view(torch.int32), t2.view(torch.int32))
+    # and against the oracle's float64 mean on a slice
+    ref = osweep.times(model, vl, begin, begin + min(4096, end - begin))
+    assert rel_err(d1[:len(ref)].cpu().numpy(), ref, model["y_scale"]).max() <= TOL[prec]
