@@ -44,7 +44,12 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1, "us": 1e-
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Rows of `ncu -i <rep> --page raw --csv`; a `.raw.csv` file exported on
+    the GPU box (the .ncu-rep files exceed gpurun's copy-back limit) is read as is."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -92,7 +97,7 @@ def main():
     summary = json.load(open(js_path)) if os.path.exists(js_path) else {}
     md = [f"# ncu summary ({a.tag})", ""]
     for rep in a.full:
-        m = re.search(r"prof\w*?_([a-z0-9]+)_([a-z0-9]+)\.ncu-rep$", os.path.basename(rep))
+        m = re.search(r"prof\w*?_([a-z0-9]+)_([a-z0-9]+)\.(?:ncu-rep|raw\.csv)$", os.path.basename(rep))
         key = f"{m.group(1)}/{m.group(2)}" if m else os.path.basename(rep)
         for d in raw(rep):
             if "sweep_kernel" not in d["kernel"]:
