@@ -256,6 +256,7 @@ struct KernelInfo {
   bool ens_pair = false;   // single-pass ensemble on CTA pairs (cluster of 2, 128-row tiles, members split)
   uint32_t w_mult = 1;     // member images resident per CTA (weight region = w_mult x w_bytes)
   uint32_t xch_bytes = 0;  // shared-memory exchange buffers (ensemble pairs)
+  const void* fn_topk = nullptr;  // MODE_TOPK-only instantiation of fn (null: fn serves every mode)
 };
 
 template <int H, int SPG, int PREC>
@@ -313,9 +314,14 @@ KernelInfo kinfo8() {
   // 1-2 % faster than CB = 16 (cfg2 3.49e10 vs 3.46e10, cfg5 3.15e10 vs 3.09e10
   // evals/s, same box); SURR_K8CB=16 selects the other split for A/B
   const char* v = getenv("SURR_K8CB");
-  const void* fn = (v && atoi(v) == 16) ? (const void*)&sweep_kernel8<H, SPG, PREC, 16>
-                                        : (const void*)&sweep_kernel8<H, SPG, PREC, 0>;
+  const bool cb16 = v && atoi(v) == 16;
+  const void* fn = cb16 ? (const void*)&sweep_kernel8<H, SPG, PREC, 16>
+                        : (const void*)&sweep_kernel8<H, SPG, PREC, 0>;
   KernelInfo ki{fn, 4, 512, true};
+  // the sweep's own instantiation (mode fixed to MODE_TOPK at compile time;
+  // SURR_K8_ANYMODE=1 runs the any-mode kernel for A/B)
+  const char* am = getenv("SURR_K8_ANYMODE");
+  if (!cb16 && !(am && atoi(am) == 1)) ki.fn_topk = (const void*)&sweep_kernel8<H, SPG, PREC, 0, MODE_TOPK>;
   ki.a0_smem = true;  // SS-form A0 tiles + the bias ones block in shared memory
   return ki;
 }
@@ -704,7 +710,8 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
 }
 
 surr_status launch(surrogate* h, Launch& L, int mode, cudaStream_t st) {
-  CU(cudaFuncSetAttribute(L.ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+  const void* fn = (mode == MODE_TOPK && L.ki.fn_topk) ? L.ki.fn_topk : L.ki.fn;
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->timing) {  // every K1 launch (ensembles run one per member)
     if (h->ev_used + 2 > h->ev.size()) {
@@ -733,9 +740,9 @@ surr_status launch(surrogate* h, Launch& L, int mode, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CU(cudaLaunchKernelExC(&cfg, L.ki.fn, args));
+    CU(cudaLaunchKernelExC(&cfg, fn, args));
   } else {
-    CU(cudaLaunchKernel(L.ki.fn, dim3(L.grid), dim3(L.ki.threads), args, L.smem, st));
+    CU(cudaLaunchKernel(fn, dim3(L.grid), dim3(L.ki.threads), args, L.smem, st));
   }
   if (e1) CU(cudaEventRecord(e1, st));
   ++h->launches;

@@ -53,8 +53,11 @@ __device__ __forceinline__ float fin_sum(const uint64_t (&acc)[4]) {
 // CB: columns of half b carried into the next iteration (16: the 48 others in
 // the L1 shadow; 0: all of half b in the L1 shadow, so the epilogue can load
 // 64 columns per TMEM wait within the register budget)
-template <int H, int SPG, int PREC, int CB = 16>
-__global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ KParams p, int mode) {
+// FM: the mode fixed at compile time (MODE_TOPK: the sweep itself, no dense /
+// operand-dump code or per-tile mode tests), or -1 (any mode, at run time)
+template <int H, int SPG, int PREC, int CB = 16, int FM = -1>
+__global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ KParams p, int mode_rt) {
+  const int mode = FM >= 0 ? FM : mode_rt;
   constexpr int EC = CB == 0 ? 2 : 1;  // 32-column chunks per TMEM load wait in epilogue 1
   constexpr int NG = K0 / SPG;
   constexpr int NSLOT = 4;
@@ -113,7 +116,8 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
   const uint32_t row = wq * 32u + lane;
   const uint32_t dslot = tmem_base + s * H;                 // lane 0 view (UMMA operands)
   const uint32_t dcol = dslot + ((wq * 32u) << 16);          // this warp's lanes
-  uint8_t* a0tile = smem + p.smem_a0 + s * 4096u;
+  // this row's place in the slot's A0 tile (K-major core matrices, st_a0_smem's layout)
+  const uint32_t a0_st = smem_u32(smem + p.smem_a0 + s * 4096u) + (row >> 3) * 256u + (row & 7u) * 16u;
   const uint8_t* slut = smem + p.smem_lut;
   surr_record* mycand = ts.cand + (size_t)warp * CAND_CAP;
   uint32_t ncand = 0;
@@ -151,8 +155,9 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
   auto store_a0 = [&](const uint32_t (&D)[MAXG], uint64_t Ir) {
     A0Regs a0;
     if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC>(p, slut, D, a0);
-    a0_dump<false>(p, mode, a0, Ir);
-    st_a0_smem(a0tile, row, a0.hi);
+    if (FM != MODE_TOPK) a0_dump<false>(p, mode, a0, Ir);
+    st_shared_v4(a0_st, a0.hi[0], a0.hi[1], a0.hi[2], a0.hi[3]);
+    st_shared_v4(a0_st + 128u, a0.hi[4], a0.hi[5], a0.hi[6], a0.hi[7]);
     fence_proxy_async_smem();
   };
   // a tile's prediction is final: top-k / dense output

@@ -9,32 +9,35 @@
 // runs its tile through its GM members back to back — the A0 tile stays in
 // shared memory across them, only the weight descriptors change — with the
 // schedule of sweep_kernel8 (final layer pipelined across the units
-// (tile, member)).  Rank 1 sends its GM per-member predictions of a row to rank
-// 0 with one st.async (16 bytes, completing on rank 0's mbarrier); rank 0 adds
-// them after its own in member order e = 0 .. E-1 (the summation order of the
+// (tile, member)).  Tiles alternate between the ranks as the one that
+// finishes them: on even tiles rank 1 sends its GM per-member predictions of a
+// row to rank 0 with one st.async (16 bytes, completing on rank 0's mbarrier),
+// on odd tiles rank 0 sends its ordered partial sum to rank 1; the receiver
+// continues the sum in member order e = 0 .. E-1 (the summation order of the
 // multi-pass path and of predict, so t is bitwise the same), divides by E and
-// runs the top-k.  Exchange buffers are double-buffered per slot (full: rank
-// 0, tx-counted; empty: rank 1, arrived remotely by rank 0).
+// runs the top-k.  Per slot, exchange buffer b carries the tiles rank b
+// finishes (full: on rank b, tx-counted; empty: on the sender, arrived
+// remotely by rank b).
 #pragma once
 #include "sweep_kernel8.cuh"
 
 namespace surr {
 
-// final-layer FFMA2 step with the member's weights from shared memory (the
-// image's w' = y_scale w / 2 floats; broadcast loads)
-__device__ __forceinline__ void relu_dot2_s(const float* w, uint32_t v0, uint32_t v1, int n, uint64_t (&acc)[4],
-                                            int j) {
-  const float2 ww = *reinterpret_cast<const float2*>(w + n);
-  const uint64_t w2 = pack2(ww.x, ww.y);
-  const float x0 = __uint_as_float(v0), x1 = __uint_as_float(v1);
-  acc[(j >> 1) & 1] = ffma2(w2, pack2(x0, x1), acc[(j >> 1) & 1]);
-  acc[2 + ((j >> 1) & 1)] = ffma2(w2, pack2(fabsf(x0), fabsf(x1)), acc[2 + ((j >> 1) & 1)]);
-}
+// final-layer FFMA2 steps with the member's weights w' = y_scale w / 2 from its
+// shared-memory image, four per broadcast LDS.128 (the accumulator order is
+// final_compute's, so t is bitwise the single-net path's)
 template <int NC>
-__device__ __forceinline__ float final_compute_s(const float* w, const uint32_t (&v)[64], int n0) {
+__device__ __forceinline__ float final_compute_c(const float* w, const uint32_t (&v)[64], int n0) {
   uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-  for (int j = 0; j < NC; j += 2) relu_dot2_s(w, v[j], v[j + 1], n0 + j, acc, j);
+  for (int j = 0; j < NC; j += 4) {
+    const float4 w4 = *reinterpret_cast<const float4*>(w + n0 + j);
+    const uint64_t wa = pack2(w4.x, w4.y), wb = pack2(w4.z, w4.w);
+    acc[0] = ffma2(wa, pack2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])), acc[0]);
+    acc[2] = ffma2(wa, pack2(fabsf(__uint_as_float(v[j])), fabsf(__uint_as_float(v[j + 1]))), acc[2]);
+    acc[1] = ffma2(wb, pack2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])), acc[1]);
+    acc[3] = ffma2(wb, pack2(fabsf(__uint_as_float(v[j + 2])), fabsf(__uint_as_float(v[j + 3]))), acc[3]);
+  }
   return fin_sum(acc);
 }
 
@@ -49,8 +52,8 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
   const uint32_t rank = cluster_ctarank();
   const uint32_t pair = blockIdx.x >> 1;
 
-  // bars: [0] load, [4 + s] slot s MMAs, [32 + 2s + b] exchange full (rank 0),
-  // [40 + 2s + b] exchange empty (rank 1)
+  // bars: [0] load, [4 + s] slot s MMAs, [32 + 2s + b] exchange full (on rank b),
+  // [40 + 2s + b] exchange empty (on rank 1 - b)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_misc);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + p.smem_misc + 64);
   TopkShared ts;
@@ -77,8 +80,9 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
       for (uint32_t off = 0; off < wbytes; off += 32768u)
         bulk_g2s(smem + off, wsrc + off, min(32768u, wbytes - off), &bars[0]);
       if (p.lut_bytes) bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[0]);
-      if (rank == 0)  // arm every exchange buffer's first use
-        for (int i = 0; i < 2 * NSLOT; ++i) mbar_arrive_expect_tx(&bars[32 + i], XBYTES);
+      // arm the first use of every exchange buffer this CTA receives (b = rank)
+      for (int i = 0; i < 2 * NSLOT; ++i)
+        if ((uint32_t)(i & 1) == rank) mbar_arrive_expect_tx(&bars[32 + i], XBYTES);
     }
     __syncwarp();
     tmem_alloc<512>(tmem_slot);
@@ -156,39 +160,50 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
     fence_proxy_async_smem();
   };
 
-  // per-tile member predictions: rank 0 keeps the running sum in member order,
-  // rank 1 its GM values for the exchange
+  // per-tile member predictions: each rank keeps its members' running sum in
+  // member order and the values themselves.  The tiles alternate between the
+  // ranks as the one that finishes them (sums, divides by E, runs the top-k):
+  // exchange buffer b = tseq & 1 always flows towards rank b, so the finishing
+  // work and the release / acquire handshakes are split evenly between the two
+  // CTAs (rank 1 used to idle on rank 0's handshake).  Rank 1 sends its GM
+  // values, rank 0 its ordered partial sum; the receiver continues the sum in
+  // member order e = 0 .. E-1 either way (bitwise the multi-pass order).
   float tsum = 0.0f;
   float tm[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-  uint32_t tseq = 0;  // tiles completed by this slot (exchange buffer = tseq & 1)
+  uint32_t tseq = 0;  // tiles completed by this slot
   // unit (tile, member m) is final: t_m = dot + c_m; on the tile's last member,
-  // exchange and (rank 0) emit
+  // exchange and (receiver) emit
   auto unit_done = [&](float dot, uint32_t m, uint64_t Ir) {
     const float t = dot + p.ens_c[rank * GM + m];
-    if (rank == 0) {
-      tsum = m == 0 ? t : tsum + t;
-    } else {
+    tsum = m == 0 ? t : tsum + t;
 #pragma unroll
-      for (int i = 0; i < GM; ++i) tm[i] = (uint32_t)i == m ? t : tm[i];  // (registers, not a local array)
-    }
+    for (int i = 0; i < GM; ++i) tm[i] = (uint32_t)i == m ? t : tm[i];  // (registers, not a local array)
     if (m + 1 < GM) return;
     const uint32_t b = tseq & 1u, q = tseq >> 1;
     float4* xb = xbuf + (s * 2 + b) * TILE_M;
-    if (rank == 1) {
-      mbar_wait_cluster(&bars[40 + 2 * s + b], (q & 1u) ^ 1u);  // rank 0 has read this buffer's last use
-      st_async_v4(&xb[row], tm[0], tm[1], tm[2], tm[3], &bars[32 + 2 * s + b], 0);
+    if (rank != b) {  // sender: buffer b's previous use has been read by rank b
+      mbar_wait_cluster(&bars[40 + 2 * s + b], (q & 1u) ^ 1u);
+      if (rank == 1) st_async_v4(&xb[row], tm[0], tm[1], tm[2], tm[3], &bars[32 + 2 * s + b], 0);
+      else st_async_v4(&xb[row], tsum, 0.0f, 0.0f, 0.0f, &bars[32 + 2 * s + b], 1);
     } else {
       mbar_wait_cluster(&bars[32 + 2 * s + b], q & 1u);
       const float4 u = xb[row];
-      float acc = tsum;
-      const float uu[4] = {u.x, u.y, u.z, u.w};
+      float acc;
+      if (rank == 0) {  // members GM .. 2 GM - 1 after this CTA's ordered partial
+        acc = tsum;
+        const float uu[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-      for (int i = 0; i < GM; ++i) acc = acc + uu[i];  // members GM .. 2 GM - 1, in order
+        for (int i = 0; i < GM; ++i) acc = acc + uu[i];
+      } else {  // rank 0's ordered partial, then this CTA's members in order
+        acc = u.x;
+#pragma unroll
+        for (int i = 0; i < GM; ++i) acc = acc + tm[i];
+      }
       const float tt = acc * p.inv_e;
       named_bar_sync(bar_id, 128);  // every row of the buffer read
       if (wq == 0 && lane == 0) {
         mbar_arrive_expect_tx(&bars[32 + 2 * s + b], XBYTES);  // arm its next use
-        mbar_arrive_cluster(&bars[40 + 2 * s + b], 1);         // and hand it back to rank 1
+        mbar_arrive_cluster(&bars[40 + 2 * s + b], rank ^ 1u);  // and hand it back to the sender
       }
       const bool valid = Ir < p.end;
       if (mode == MODE_TOPK) topk_offer(ts, mycand, ncand, valid, tt, Ir, p.k, lane);
@@ -252,7 +267,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
         uint32_t v[64];
         final_load<H / 2>(dcol + H / 2, v);
         issue(2, m);
-        pa = final_compute_s<H / 2>(fin_w(m), v, 0);
+        pa = final_compute_c<H / 2>(fin_w(m), v, 0);
       }
       // ---- L2b done: half b, next unit's L1 (same A0 with the next member, or the next tile's)
       mbar_wait(&bars[4 + s], ph);
@@ -263,7 +278,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
         final_load<H / 2>(dcol + H / 2, v);
         if (!last_m) issue(0, m + 1);
         else if (has_next) issue(0, 0);
-        pdot = pa + final_compute_s<H / 2>(fin_w(m), v, H / 2);
+        pdot = pa + final_compute_c<H / 2>(fin_w(m), v, H / 2);
       }
       pm = m;
       pI = I;
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
     lock_release(ts, lane);
   }
 
-  // ---- teardown (rank 1's list stays all sentinels: rank 0 owns the tiles' top-k)
+  // ---- teardown (each CTA's list holds the tiles it finished)
   tc_fence_before();
   __syncthreads();
   if (mode == MODE_TOPK) {
