@@ -81,7 +81,7 @@ struct surrogate {
   surr_record* d_merged = nullptr;
   uint64_t* d_idx = nullptr;
   float* d_t = nullptr;
-  uint32_t* d_ctr = nullptr;    // ticket of the fused grid merge (zero between launches)
+  uint32_t* d_ctr = nullptr;    // tickets of the fused grid merge tree (zero between launches)
   uint32_t* a0_dump = nullptr;  // MODE_A0 output of the current call
   uint64_t a0_stride = 1;
   // debug timeline
@@ -475,6 +475,8 @@ size_t smem_layout(const KernelInfo& ki, KParams& p, uint32_t lut_bytes, uint32_
   return off;
 }
 constexpr size_t SMEM_MAX = 227 * 1024;
+// fused grid-merge tree: one ticket per node, TREE_NODES_PER_LEVEL per level, up to 9 levels (grid <= 256)
+constexpr size_t CTR_BYTES = 9 * TREE_NODES_PER_LEVEL * sizeof(uint32_t);
 
 // ------------------------------------------------------------ space / LUT
 surr_status f16_range_check(surrogate* h, const std::vector<uint32_t>& radix, const std::vector<double>& values);
@@ -780,7 +782,7 @@ surr_status launch_merge(surrogate* h, const surr_record* in, uint32_t lists, ui
 // chunk of <= 2^28 configs, members 0..E-2 accumulate t into d_acc and the last
 // member averages and emits (top-k records at recs + lists * k, or dense t,
 // or predict rows).  Returns the number of record lists written.
-// Merged top-k outputs of a sweep; K1 merges its own lists (last CTA, a9) when
+// Merged top-k outputs of a sweep; K1 merges its own lists (a9: a binary tree of CTAs) when
 // the sweep is a single top-k launch whose shared memory holds the merge.
 struct MergeOut {
   uint64_t* idx;
@@ -808,12 +810,11 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
       L.p.a0_stride = h->a0_stride;
       L.p.trace = h->trace;
       L.p.trace_n = h->trace_n;
-      const size_t need1 = 4ull * k * sizeof(surr_record);
-      const bool fuse = mo && mode == MODE_TOPK && L.smem >= need1 && !getenv("SURR_NO_FUSED_MERGE");
+      const size_t need1 = 3ull * k * sizeof(surr_record);  // the merge tree's two lists + result
+      const bool fuse = mo && mode == MODE_TOPK && L.smem >= need1 && L.grid <= (int)TREE_NODES_PER_LEVEL &&
+                        !getenv("SURR_NO_FUSED_MERGE");
       if (fuse) {
         L.p.done_ctr = h->d_ctr;
-        L.p.merge_chunk = std::min<uint32_t>(
-            (uint32_t)((L.smem - 2ull * k * sizeof(surr_record)) / (2ull * k * sizeof(surr_record))), (uint32_t)L.grid);
         L.p.out_idx = mo->idx;
         L.p.out_t = mo->t;
         L.p.out_recs = mo->recs;
@@ -829,15 +830,15 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
   const uint64_t chunk = E == 1 ? (end - begin) : (1ull << 28);
   // record lists of every chunk's final pass
   uint64_t lists = 0, nchunks = 0;
-  uint32_t fuse_chunk = 0;  // lists per merge pass of a fused merge (0: K2 merges)
+  uint32_t fuse_chunk = 0;  // 1: K1 can merge its grid's lists itself (a9 tree), 0: K2 merges
   for (uint64_t c0 = begin; c0 < end; c0 += chunk) {
     Launch L;
     surr_status rc = plan(h, c0, std::min(end, c0 + chunk), k, mode, &L);
     if (rc) return rc;
     lists += (uint64_t)L.grid;
     ++nchunks;
-    const size_t need1 = 4ull * k * sizeof(surr_record);  // 2 k result + one list pair of 2 k
-    if (L.smem >= need1) fuse_chunk = (uint32_t)((L.smem - 2ull * k * sizeof(surr_record)) / (2ull * k * sizeof(surr_record)));
+    const size_t need1 = 3ull * k * sizeof(surr_record);  // the merge tree's two lists + result
+    if (L.smem >= need1 && L.grid <= (int)TREE_NODES_PER_LEVEL) fuse_chunk = 1;
   }
   const bool fuse = mo && mode == MODE_TOPK && nchunks == 1 && fuse_chunk >= 1 && !getenv("SURR_NO_FUSED_MERGE");
   if (mo) mo->fused = fuse;
@@ -876,7 +877,6 @@ surr_status run_k1(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int m
       L.p.recs = h->d_recs + done * k;
       if (fuse && last) {
         L.p.done_ctr = h->d_ctr;
-        L.p.merge_chunk = std::min<uint32_t>(fuse_chunk, (uint32_t)L.grid);
         L.p.out_idx = mo->idx;
         L.p.out_t = mo->t;
         L.p.out_recs = mo->recs;
@@ -920,7 +920,7 @@ surr_status sweep_common(surrogate* h, const surr_space* space, uint32_t k, uint
   MergeOut mo{idx_dev, t_dev, recs_dev};
   rc = run_k1(h, begin, end, k, MODE_TOPK, nullptr, nullptr, st, &lists, &mo);
   if (rc) return rc;
-  if (mo.fused) return SURR_OK;  // K1's last CTA merged the grid's lists (a9): one kernel per sweep
+  if (mo.fused) return SURR_OK;  // K1 merged its grid's lists (a9 tree): one kernel per sweep
   return launch_merge(h, h->d_recs, lists, k, k, idx_dev, t_dev, recs_dev, st);
 }
 
@@ -940,7 +940,7 @@ surr_status surrogate_create(int cuda_device, surrogate_t** out) {
   if (cudaSetDevice(cuda_device) != cudaSuccess) { delete h; return fail(nullptr, SURR_E_CUDA, "cudaSetDevice"); }
   cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cuda_device);
   if (cudaMalloc(&h->d_merged, SURR_K_MAX * sizeof(surr_record)) != cudaSuccess ||
-      cudaMalloc(&h->d_ctr, 64) != cudaSuccess || cudaMemset(h->d_ctr, 0, 64) != cudaSuccess) {
+      cudaMalloc(&h->d_ctr, CTR_BYTES) != cudaSuccess || cudaMemset(h->d_ctr, 0, CTR_BYTES) != cudaSuccess) {
     cudaFree(h->d_merged);
     delete h;
     return fail(nullptr, SURR_E_OOM, "cudaMalloc");

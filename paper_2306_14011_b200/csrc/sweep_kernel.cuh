@@ -95,10 +95,9 @@ struct KParams {
   // outputs
   uint32_t k;
   surr_record* recs;         // MODE_TOPK: gridDim.x * k records
-  // fused grid merge (a9 in K1, MODE_TOPK): ticket counter (null: K2 merges),
-  // merge chunk (lists per shared-memory pass), merged outputs
+  // fused grid merge (a9 in K1, MODE_TOPK): per-node tickets of the CTA merge
+  // tree (null: K2 merges), merged outputs
   uint32_t* done_ctr;
-  uint32_t merge_chunk;
   uint64_t* out_idx;
   float* out_t;
   surr_record* out_recs;
@@ -248,7 +247,7 @@ __device__ __forceinline__ void odometer_step(const uint32_t* R, const uint32_t*
 struct TopkShared {
   surr_record* lists;  // [2][k]
   surr_record* cand;   // [num epilogue warps][CAND_CAP]
-  volatile uint32_t* misc;  // [0] lock, [1] cur, [2] thr_key, [3..4] thr_idx
+  volatile uint32_t* misc;  // [0] lock, [1] cur, [2] thr_key, [3..4] thr_idx, [5] valid entries of the list
 };
 
 __device__ __forceinline__ uint32_t lower_bound_recs(const surr_record* a, uint32_t n, uint32_t key, uint64_t idx) {
@@ -271,7 +270,13 @@ __device__ __forceinline__ uint32_t upper_bound_recs_fwd(const surr_record* a, u
   return lo;
 }
 
-// Merge the warp's cnt candidates into the CTA list (caller holds the lock).
+// Merge the warp's cnt (<= CAND_CAP) candidates into the CTA list (caller
+// holds the lock).  misc[5] = nv, the list's valid prefix (L[nv..k) are
+// sentinels, candidates never are), so the work is O(nv + cnt), not O(k),
+// while the list fills.  Every candidate's insertion point ub_j = #{L < c_j}
+// comes from one binary search over L; the candidates are written, then the
+// ub_j (ascending) replace them in the warp's buffer as a compact word array
+// and each lane walks its L elements' shifts #{j : ub_j <= i} with a pointer.
 __device__ void warp_merge(TopkShared& ts, surr_record* cand, uint32_t cnt, uint32_t k, uint32_t lane) {
   // 1. sort candidates by rank (all keys distinct: idx unique)
   surr_record c0, c1;
@@ -284,28 +289,35 @@ __device__ void warp_merge(TopkShared& ts, surr_record* cand, uint32_t cnt, uint
     if (h0 && rec_less(o.key, o.idx, c0.key, c0.idx)) ++r0;
     if (h1 && rec_less(o.key, o.idx, c1.key, c1.idx)) ++r1;
   }
-  __syncwarp();
-  if (h0) cand[r0] = c0;
-  if (h1) cand[r1] = c1;
-  __syncwarp();
-  // 2. rank merge with the sorted list, keep the first k
-  uint32_t cur = ts.misc[1];
+  // 2. insertion points in the valid prefix of L
+  const uint32_t cur = ts.misc[1];
+  const uint32_t nv = ts.misc[5];
   surr_record* L = ts.lists + (size_t)cur * k;
   surr_record* O = ts.lists + (size_t)(cur ^ 1u) * k;
-  for (uint32_t i = lane; i < k; i += 32) {
-    surr_record e = L[i];
-    uint32_t p = i + lower_bound_recs(cand, cnt, e.key, e.idx);
-    if (p < k) O[p] = e;
+  const uint32_t u0 = h0 ? upper_bound_recs_fwd(L, nv, c0.key, c0.idx) : 0u;
+  const uint32_t u1 = h1 ? upper_bound_recs_fwd(L, nv, c1.key, c1.idx) : 0u;
+  if (nv == 0) {  // first merge: the second buffer's tail becomes sentinels once
+    for (uint32_t i = cnt + lane; i < k; i += 32) { O[i].idx = IDX_SENT; O[i].key = KEY_SENT; O[i].pad = 0; }
   }
-  for (uint32_t j = lane; j < cnt; j += 32) {
-    surr_record c = cand[j];
-    uint32_t p = j + upper_bound_recs_fwd(L, k, c.key, c.idx);
-    if (p < k) O[p] = c;
+  // 3. candidates to their final places (rank + insertion point)
+  if (h0 && r0 + u0 < k) { c0.pad = 0; O[r0 + u0] = c0; }
+  if (h1 && r1 + u1 < k) { c1.pad = 0; O[r1 + u1] = c1; }
+  __syncwarp();
+  uint32_t* ub = reinterpret_cast<uint32_t*>(cand);  // the candidates are placed: reuse the buffer
+  if (h0) ub[r0] = u0;
+  if (h1) ub[r1] = u1;
+  __syncwarp();
+  // 4. L's valid elements shift by the number of candidates inserted before them
+  uint32_t jp = 0;
+  for (uint32_t i = lane; i < nv; i += 32) {
+    while (jp < cnt && ub[jp] <= i) ++jp;
+    if (i + jp < k) O[i + jp] = L[i];
   }
   __syncwarp();
   if (lane == 0) {
     surr_record last = O[k - 1];
     ts.misc[1] = cur ^ 1u;
+    ts.misc[5] = min(nv + cnt, k);
     ts.misc[3] = (uint32_t)last.idx;
     ts.misc[4] = (uint32_t)(last.idx >> 32);
     ts.misc[2] = last.key;
@@ -363,7 +375,7 @@ __device__ __forceinline__ void rank_merge(const surr_record* A, uint32_t na, co
 
 // The merge body, run by every thread of one CTA over `sm` (shared memory of
 // (2 k + 2 chunk max(k_in, k)) records).  CG: read the lists with ld.global.cg
-// (written by other CTAs of the same launch: the fused last-CTA merge).
+// (written by other CTAs of the same launch).
 template <bool CG>
 __device__ void merge_lists(const surr_record* __restrict__ in, uint32_t lists, uint32_t k_in, uint32_t k,
                             uint32_t chunk, uint64_t* out_idx, float* out_t, surr_record* out_recs, uint8_t* sm) {
@@ -432,23 +444,74 @@ __global__ void __launch_bounds__(1024, 1)
   merge_lists<false>(in, lists, k_in, k, chunk, out_idx, out_t, out_recs, sm);
 }
 
-// a9 fused into K1 (MODE_TOPK, p.done_ctr set): every CTA has written its k
-// records to p.recs[blockIdx.x k ..]; the last CTA to finish (device-scope
-// ticket) merges all gridDim.x lists into the outputs with the same code as
-// K2, reusing its shared memory, and re-arms the ticket for the next launch.
-// Called by every thread of the CTA after the kernel's teardown.
+// a9 fused into K1 (MODE_TOPK, p.done_ctr set) as a binary tree of CTAs: every
+// CTA has written its k records to p.recs[blockIdx.x k ..]; at level l the
+// node j covers CTAs [j 2^l, (j + 1) 2^l) and its list sits in the slot of its
+// leftmost CTA (j 2^l).  Of the two children of a node, the one that finishes
+// second (device-scope ticket per node, re-armed by that CTA) merges both
+// lists (staged in its shared memory) into the left child's slot and climbs;
+// the other one exits.  A node without a sibling (odd count) climbs without a
+// merge.  The CTA that completes the root writes the outputs.  The critical
+// path is log2(grid) two-list merges (~8 at 148 CTAs) instead of one CTA
+// merging every list (the chunked K2 loop: ~1 ms at k = 1024, measured).
+// Ties (only sentinels can tie) keep list order, so the result is the unique
+// (key, idx) top-k.  Called by every thread of the CTA after the teardown.
+constexpr uint32_t TREE_NODES_PER_LEVEL = 256;  // ticket array: levels x 256 counters (grid <= 256)
 __device__ __forceinline__ void grid_merge_tail(const KParams& p, int mode, uint8_t* sm) {
   if (mode != MODE_TOPK || p.done_ctr == nullptr) return;
-  __syncthreads();  // this CTA's records are written (and its shared memory is free)
-  int last = 0;
-  if (threadIdx.x == 0) {
-    __threadfence();  // release: the records before the ticket
-    last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
-    if (last) __threadfence();  // acquire: every other CTA's records
+  const uint32_t k = p.k, t = threadIdx.x, nt = blockDim.x;
+  surr_record* A = reinterpret_cast<surr_record*>(sm);
+  surr_record* B = A + k;
+  surr_record* O = B + k;
+  uint32_t node = blockIdx.x, nodes = gridDim.x, l = 0;
+  bool merged = false;  // O holds this CTA's latest merge result
+  for (; nodes > 1; ++l) {
+    if ((node ^ 1u) < nodes) {
+      __syncthreads();  // this CTA's list (or merge result) is written
+      int second = 0;
+      if (t == 0) {
+        uint32_t* tk = p.done_ctr + l * TREE_NODES_PER_LEVEL + (node >> 1);
+        __threadfence();  // release: the list before the ticket
+        second = atomicAdd(tk, 1u) == 1u;
+        if (second) {
+          __threadfence();  // acquire: the sibling's list
+          *tk = 0u;         // re-armed for the next launch (nobody else touches it in this one)
+        }
+      }
+      if (!__syncthreads_or(second)) return;  // the sibling merges
+      const surr_record* L = p.recs + (size_t)((node & ~1u) << l) * k;
+      const surr_record* R = p.recs + (size_t)((node | 1u) << l) * k;
+      for (uint32_t i = t; i < k; i += nt) {
+        reinterpret_cast<uint4*>(A)[i] = __ldcg(reinterpret_cast<const uint4*>(L) + i);
+        reinterpret_cast<uint4*>(B)[i] = __ldcg(reinterpret_cast<const uint4*>(R) + i);
+      }
+      __syncthreads();
+      rank_merge(A, k, B, k, O, k, t, nt);
+      __syncthreads();
+      merged = true;
+      if (nodes > 2) {  // not the root: the result goes to the parent's slot (= the left child's)
+        surr_record* P = p.recs + (size_t)((node & ~1u) << l) * k;
+        for (uint32_t i = t; i < k; i += nt) reinterpret_cast<uint4*>(P)[i] = reinterpret_cast<const uint4*>(O)[i];
+      }
+    }
+    node >>= 1;
+    nodes = (nodes + 1) >> 1;
   }
-  if (!__syncthreads_or(last)) return;
-  merge_lists<true>(p.recs, gridDim.x, p.k, p.k, p.merge_chunk, p.out_idx, p.out_t, p.out_recs, sm);
-  if (threadIdx.x == 0) *p.done_ctr = 0u;  // re-armed (launches on one handle are stream-ordered)
+  // the root: this CTA's merge result (or, grid of one, its own list)
+  __syncthreads();
+  const surr_record* src = merged ? O : p.recs + (size_t)blockIdx.x * k;
+  for (uint32_t i = t; i < k; i += nt) {
+    surr_record e;
+    if (merged) {
+      e = src[i];
+    } else {
+      const uint4 u = __ldcg(reinterpret_cast<const uint4*>(src) + i);
+      e = *reinterpret_cast<const surr_record*>(&u);
+    }
+    if (p.out_idx) p.out_idx[i] = e.idx;
+    if (p.out_t) p.out_t[i] = key2f(e.key);
+    if (p.out_recs) p.out_recs[i] = e;
+  }
 }
 
 // A0 operand of one row: bf16 / fp16 -> 8 packed columns; 3xFP16 -> 8 hi + 8 lo
@@ -599,7 +662,7 @@ __global__ void __launch_bounds__(Cfg<PREC, H>::THREADS, 1)
       ts.lists[i].pad = 0;
     }
     if (lane == 0) {
-      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu;
+      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu; ts.misc[5] = 0;
     }
   }
   tc_fence_before();

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
       ts.lists[i].pad = 0;
     }
     if (lane == 0) {
-      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu;
+      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu; ts.misc[5] = 0;
     }
   }
   if (warp < 4) {  // the bias ones block (row-constant [1, 0, ...]) of the layer-2 bias K step

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(CfgPair<H, NS>::THREADS, 1)
       ts.lists[i].pad = 0;
     }
     if (lane == 0) {
-      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu;
+      ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu; ts.misc[5] = 0;
     }
   }
   if (warp >= 4 && warp < 8) {  // constant ones tile of the bias K step (bf16 1.0 in K slot 0)

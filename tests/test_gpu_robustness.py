@@ -143,10 +143,18 @@ def test_table_and_weight_swaps_while_sweeps_are_queued(pk):
     ("cfg2", "cfg4_17-128-128-1_x8", "fp16", 16, 0, 1 << 22),
     ("tiny", "tiny_14-32-32-1", "fp32", 1, 0, None),
     ("cfg2", "cfg2_14-128-128-1", "fp16", 1024, 0, 3000),   # fewer configs than a full grid of lists
+    # odd and tiny grids of the merge tree (4 tiles of 128 rows per CTA): 37, 3, 2, 1 CTAs
+    ("cfg2", "cfg2_14-128-128-1", "fp16", 64, 0, 512 * 37 - 5),
+    ("cfg2", "cfg2_14-128-128-1", "fp16", 1024, 10, 10 + 512 * 3),
+    ("cfg2", "cfg2_14-128-128-1", "bf16", 7, 99, 99 + 512 * 2),
+    ("cfg2", "cfg2_14-128-128-1", "fp16", 5, 123, 123 + 300),
+    ("cfg5", "cfg5_14-128-128-1", "fp16", 1000, 7, 7 + 512 * 147 + 1),  # 148 CTAs, the last one a single row
 ])
 def test_fused_grid_merge_equals_k2(pk, monkeypatch, name, weights, prec, k, begin, end):
-    """a9 in K1 (last CTA merges the grid's lists) == K1 + the separate K2 merge,
-    bitwise, and the sweep is one kernel launch."""
+    """a9 in K1 (a binary tree of CTAs merges the grid's lists) == K1 + the
+    separate K2 merge, bitwise, and the sweep is one kernel launch; odd grids
+    (nodes without a sibling), a grid of one and repeated launches (tickets
+    re-armed) included."""
     import torch
     vl = workloads.space(name)
     model = workloads.load_model(weights)
