@@ -195,6 +195,7 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     }
     if (lane == 0) {
       ts.misc[0] = 0; ts.misc[1] = 0; ts.misc[2] = KEY_SENT; ts.misc[3] = 0xFFFFFFFFu; ts.misc[4] = 0xFFFFFFFFu; ts.misc[5] = 0;
+      for (uint32_t b = 0; b < TOPK_MAX_BUFS; ++b) ts.misc[8 + b] = 0;
     }
   }
   tc_fence_before();
@@ -455,16 +456,14 @@ __global__ void __launch_bounds__(Cfg3<H, NS>::THREADS, 1)
     if (tr) trace_ev(p, s, jr, 7);
     I = In;
   }
-  if (mode == MODE_TOPK && ncand) {
-    lock_acquire(ts, lane);
-    warp_merge(ts, mycand, ncand, p.k, lane);
-    lock_release(ts, lane);
-  }
+  if (mode == MODE_TOPK) topk_post(ts, mycand, ncand, lane);
 
   // ---- teardown
   tc_fence_before();
   __syncthreads();
   if (mode == MODE_TOPK) {
+    topk_drain(ts, p.k, warp, lane);
+    __syncthreads();
     const surr_record* L = ts.lists + (size_t)ts.misc[1] * p.k;
     for (uint32_t i = threadIdx.x; i < p.k; i += blockDim.x) p.recs[(size_t)blockIdx.x * p.k + i] = L[i];
   }
