@@ -81,7 +81,62 @@ __global__ void __launch_bounds__(544, 1) skel(int mode, int iters, unsigned lon
     for (int kk = 0; kk < 8; ++kk) umma_f16_ts(d, dslot + kk * 8, bd + kk * 16, idesc_f16(32), kk > 0);
     umma_f16_ss(d, d_ones, bd + 8 * 16, idesc_f16(32), 1u);
   };
-  if (mode == 9 && warp < 16) {
+  auto issue_l2b_part = [&](uint32_t s, int part) {  // L2b output neurons 32 part .. 32 part + 31 -> region 64 + 32 part
+    const uint32_t dslot = base + s * 128;
+    const uint32_t d = dslot + 64 + 32 * part;
+    const uint64_t bd = d_b2b + (uint64_t)part * 64;  // (dummy weight offsets; timing only)
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) umma_f16_ts(d, dslot + kk * 8, bd + kk * 16, idesc_f16(32), kk > 0);
+    umma_f16_ss(d, d_ones, bd + 8 * 16, idesc_f16(32), 1u);
+  };
+  if (mode == 10 && warp < 16) {
+    // kernel8 skeleton with TMEM traffic, L2b issued as two N = 32 halves: the first as
+    // soon as D2a's first 32 columns are in registers, the second after the rest
+    const uint32_t s = warp >> 2, wq = warp & 3;
+    const uint32_t dcol = base + s * 128 + ((wq * 32u) << 16);
+    uint32_t pa = 0, pb = 0, sink = 0;
+    auto sync_issue = [&](auto&& fn) {
+      tc_fence_before();
+      named_bar_sync(1 + s, 128);
+      if (wq == 0) {
+        tc_fence_after();
+        if (elect_one()) fn();
+        __syncwarp();
+      }
+    };
+    auto waitA = [&]() { mbar_wait(&bars[s], pa); pa ^= 1u; tc_fence_after(); };
+    auto waitB = [&]() { mbar_wait(&bars[8 + s], pb); pb ^= 1u; tc_fence_after(); };
+    auto ld32 = [&](uint32_t col) { uint32_t v[32]; tmem_ld32(col, v); tmem_wait_ld(); sink += v[3] + v[17]; };
+    sync_issue([&] { issue_phase(s, 0); umma_commit(&bars[s]); });
+    for (int it = 0; it < iters; ++it) {
+      waitA();  // L1
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        uint32_t v[2][32];
+        tmem_ld32(dcol + c * 32, v[0]);
+        tmem_ld32(dcol + (c + 1) * 32, v[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = v[u][2 * j] ^ v[u][2 * j + 1];
+          tmem_st16(dcol + (c + u) * 16, pk);
+        }
+      }
+      tmem_wait_st();
+      sync_issue([&] { issue_phase(s, 1); umma_commit(&bars[s]); });
+      waitA();  // L2a
+      ld32(dcol + 64);
+      sync_issue([&] { issue_l2b_part(s, 0); umma_commit(&bars[s]); });
+      ld32(dcol + 96);
+      sync_issue([&] { issue_l2b_part(s, 1); umma_commit(&bars[8 + s]); });
+      waitA(); ld32(dcol + 64);
+      waitB(); ld32(dcol + 96);
+      if (it + 1 < iters) sync_issue([&] { issue_phase(s, 0); umma_commit(&bars[s]); });
+    }
+    if (sink == 0x12345678u) out[0] = 0;
+  } else if (mode == 9 && warp < 16) {
     // L2 in four N = 32 quarters alternating between two 32-column regions, so each
     // quarter's final load overlaps the next quarter's UMMAs (TMEM traffic included)
     const uint32_t s = warp >> 2, wq = warp & 3;
@@ -261,7 +316,8 @@ int main(int argc, char** argv) {
                          "dedicated issuer warp polling slots", "dedicated issuer + TMEM traffic",
                          "skeleton + epilogue ld/st only", "skeleton + final loads only",
                          "skeleton + all TMEM traffic off the chain (after the next issue)",
-                         "L2 as four N=32 quarters in two alternating regions, with TMEM traffic"};
+                         "L2 as four N=32 quarters in two alternating regions, with TMEM traffic",
+                         "TMEM traffic, L2b as two N=32 halves issued as D2a's halves are loaded"};
   std::vector<int> modes;
   for (int i = 1; i < argc; ++i) modes.push_back(atoi(argv[i]));
   if (modes.empty()) modes = {0, 2, 6, 7};
