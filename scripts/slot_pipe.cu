@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(544, 1) skel(int mode, int iters, unsigned lon
     __syncwarp();
     tmem_alloc<512>(&tslot);
   }
-  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;
+  for (int i = threadIdx.x; i < 100 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -89,7 +89,69 @@ __global__ void __launch_bounds__(544, 1) skel(int mode, int iters, unsigned lon
     for (int kk = 0; kk < 8; ++kk) umma_f16_ts(d, dslot + kk * 8, bd + kk * 16, idesc_f16(32), kk > 0);
     umma_f16_ss(d, d_ones, bd + 8 * 16, idesc_f16(32), 1u);
   };
-  if (mode == 10 && warp < 16) {
+  // L2 half with the bias put into the accumulator by tcgen05.cp before the 8 TS UMMAs
+  // (no ones-block K step): 11 = 16 x 32x128b.warpx4 (512 B of shared memory each, broadcast
+  // to the four lane quadrants), 12 = 8 x 128x256b (4 KB each)
+  auto issue_half_cp = [&](uint32_t s, int phase, int cpmode) {
+    const uint32_t dslot = base + s * 128;
+    const uint64_t bd = phase == 1 ? d_b2a : d_b2b;
+    if (cpmode == 11) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint64_t sd = bdesc(sb + 80 * 1024 + c * 512, 128);
+        asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(dslot + 64 + c * 4), "l"(sd) : "memory");
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint64_t sd = bdesc(sb + 80 * 1024 + (c & 3) * 4096, 256);
+        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(dslot + 64 + c * 8), "l"(sd) : "memory");
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) umma_f16_ts(dslot + 64, dslot + kk * 8, bd + kk * 16, id_half, 1u);
+  };
+  if ((mode == 11 || mode == 12) && warp < 16) {
+    const uint32_t s = warp >> 2, wq = warp & 3;
+    const uint32_t dcol = base + s * 128 + ((wq * 32u) << 16);
+    uint32_t pa = 0, sink = 0;
+    auto sync_issue = [&](auto&& fn) {
+      tc_fence_before();
+      named_bar_sync(1 + s, 128);
+      if (wq == 0) {
+        tc_fence_after();
+        if (elect_one()) fn();
+        __syncwarp();
+      }
+    };
+    auto waitA = [&]() { mbar_wait(&bars[s], pa); pa ^= 1u; tc_fence_after(); };
+    auto ld64 = [&](uint32_t col) { uint32_t v[2][32]; tmem_ld32(col, v[0]); tmem_ld32(col + 32, v[1]); tmem_wait_ld(); sink += v[0][3] + v[1][17]; };
+    sync_issue([&] { issue_phase(s, 0); umma_commit(&bars[s]); });
+    for (int it = 0; it < iters; ++it) {
+      waitA();  // L1
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        uint32_t v[2][32];
+        tmem_ld32(dcol + c * 32, v[0]);
+        tmem_ld32(dcol + (c + 1) * 32, v[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pk[j] = v[u][2 * j] ^ v[u][2 * j + 1];
+          tmem_st16(dcol + (c + u) * 16, pk);
+        }
+      }
+      tmem_wait_st();
+      sync_issue([&] { issue_half_cp(s, 1, mode); umma_commit(&bars[s]); });
+      waitA(); ld64(dcol + 64);
+      sync_issue([&] { issue_half_cp(s, 2, mode); umma_commit(&bars[s]); });
+      waitA(); ld64(dcol + 64);
+      if (it + 1 < iters) sync_issue([&] { issue_phase(s, 0); umma_commit(&bars[s]); });
+    }
+    if (sink == 0x12345678u) out[0] = 0;
+  } else if (mode == 10 && warp < 16) {
     // kernel8 skeleton with TMEM traffic, L2b issued as two N = 32 halves: the first as
     // soon as D2a's first 32 columns are in registers, the second after the rest
     const uint32_t s = warp >> 2, wq = warp & 3;
@@ -308,7 +370,7 @@ __global__ void __launch_bounds__(544, 1) skel(int mode, int iters, unsigned lon
 int main(int argc, char** argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
   unsigned long long* d;
-  cudaFuncSetAttribute(skel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  cudaFuncSetAttribute(skel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaMalloc(&d, 148 * 2 * 8);
   std::vector<unsigned long long> h(148 * 2);
   const char* names[] = {"kernel8 skeleton (try_wait, named barrier, self-issue)", "same, spin test_wait",
@@ -317,7 +379,9 @@ int main(int argc, char** argv) {
                          "skeleton + epilogue ld/st only", "skeleton + final loads only",
                          "skeleton + all TMEM traffic off the chain (after the next issue)",
                          "L2 as four N=32 quarters in two alternating regions, with TMEM traffic",
-                         "TMEM traffic, L2b as two N=32 halves issued as D2a's halves are loaded"};
+                         "TMEM traffic, L2b as two N=32 halves issued as D2a's halves are loaded",
+                         "TMEM traffic, L2 bias by tcgen05.cp 32x128b.warpx4 x16 (no ones K step)",
+                         "TMEM traffic, L2 bias by tcgen05.cp 128x256b x8 (no ones K step)"};
   std::vector<int> modes;
   for (int i = 1; i < argc; ++i) modes.push_back(atoi(argv[i]));
   if (modes.empty()) modes = {0, 2, 6, 7};
@@ -325,7 +389,7 @@ int main(int argc, char** argv) {
     for (int mode : modes) {
       const int iters = 2000;
       const int threads = (mode == 4 || mode == 5) ? 544 : 512;
-      skel<<<148, threads, 96 * 1024>>>(mode, iters, d);
+      skel<<<148, threads, 100 * 1024>>>(mode, iters, d);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("mode %d error %s\n", mode, cudaGetErrorString(e)); return 1; }
       cudaMemcpy(h.data(), d, 148 * 2 * 8, cudaMemcpyDeviceToHost);
