@@ -314,14 +314,17 @@ KernelInfo kinfo8() {
   // 1-2 % faster than CB = 16 (cfg2 3.49e10 vs 3.46e10, cfg5 3.15e10 vs 3.09e10
   // evals/s, same box); SURR_K8CB=16 selects the other split for A/B
   const char* v = getenv("SURR_K8CB");
-  const bool cb16 = v && atoi(v) == 16;
-  const void* fn = cb16 ? (const void*)&sweep_kernel8<H, SPG, PREC, 16>
-                        : (const void*)&sweep_kernel8<H, SPG, PREC, 0>;
+  const bool cb16 = SPG != 0 && v && atoi(v) == 16;
+  const void* fn = (const void*)&sweep_kernel8<H, SPG, PREC, 0>;
+  if constexpr (SPG != 0)
+    if (cb16) fn = (const void*)&sweep_kernel8<H, SPG, PREC, 16>;
   KernelInfo ki{fn, 4, 512, true};
+  ki.x_stage = SPG == 0;  // the predict instantiation
   // the sweep's own instantiation (mode fixed to MODE_TOPK at compile time;
   // SURR_K8_ANYMODE=1 runs the any-mode kernel for A/B)
   const char* am = getenv("SURR_K8_ANYMODE");
-  if (!cb16 && !(am && atoi(am) == 1)) ki.fn_topk = (const void*)&sweep_kernel8<H, SPG, PREC, 0, MODE_TOPK>;
+  if constexpr (SPG != 0)
+    if (!cb16 && !(am && atoi(am) == 1)) ki.fn_topk = (const void*)&sweep_kernel8<H, SPG, PREC, 0, MODE_TOPK>;
   ki.a0_smem = true;  // SS-form A0 tiles + the bias ones block in shared memory
   return ki;
 }
@@ -390,8 +393,8 @@ bool get_kernel16(uint32_t H, uint32_t NL, KernelInfo* ki, uint32_t spg, bool en
       // 14-128-128-1 sweeps: the final layer pipelined across tiles (SURR_K3=1:
       // sweep_kernel3 for same-box A/B)
       const char* k3 = getenv("SURR_K3");
-      if (NL == 2 && spg != 0 && !(k3 && atoi(k3) == 1)) {
-        *ki = spg == 4 ? kinfo8<128, 4, PREC>() : kinfo8<128, 2, PREC>();
+      if (NL == 2 && !(k3 && atoi(k3) == 1)) {
+        *ki = spg == 4 ? kinfo8<128, 4, PREC>() : spg == 2 ? kinfo8<128, 2, PREC>() : kinfo8<128, 0, PREC>();
         return true;
       }
       *ki = spg == 4 ? kinfo3<128, 4, PREC>() : spg == 2 ? kinfo3<128, 2, PREC>() : kinfo3<128, 0, PREC>();

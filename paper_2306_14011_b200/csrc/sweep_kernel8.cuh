@@ -59,7 +59,10 @@ template <int H, int SPG, int PREC, int CB = 16, int FM = -1>
 __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ KParams p, int mode_rt) {
   const int mode = FM >= 0 ? FM : mode_rt;
   constexpr int EC = CB == 0 ? 2 : 1;  // 32-column chunks per TMEM load wait in epilogue 1
-  constexpr int NG = K0 / SPG;
+  // SPG = 0: the explicit-batch (predict) instantiation: rows from HBM instead
+  // of the decoder (bulk-copied one tile ahead into a per-slot staging buffer)
+  constexpr bool PRED = SPG == 0;
+  constexpr int NG = PRED ? 1 : K0 / SPG;
   constexpr int NSLOT = 4;
   static_assert(H == 128, "four 128-column slots");
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -78,12 +81,15 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
     if (lane == 0) {
       mbar_init(&bars[0], 1);
       for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[4 + s], 1);
+      if (PRED)
+        for (int s = 0; s < NSLOT; ++s) mbar_init(&bars[9 + s], 1);  // row staging
       fence_mbar_init();
       fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&bars[0], p.w_bytes + p.lut_bytes);
+      const uint32_t lutb = PRED ? 0u : p.lut_bytes;
+      mbar_arrive_expect_tx(&bars[0], p.w_bytes + lutb);
       for (uint32_t off = 0; off < p.w_bytes; off += 32768u)
         bulk_g2s(smem + off, (const uint8_t*)p.w_gmem + off, min(32768u, p.w_bytes - off), &bars[0]);
-      if (p.lut_bytes) bulk_g2s(smem + p.smem_lut, p.lut_gmem, p.lut_bytes, &bars[0]);
+      if (lutb) bulk_g2s(smem + p.smem_lut, p.lut_gmem, lutb, &bars[0]);
     }
     __syncwarp();
     tmem_alloc<512>(tmem_slot);
@@ -132,6 +138,22 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
   const uint64_t d_b2a = make_bdesc(sb + p.off_bh, p.sbo_bh);
   const uint64_t d_b2b = make_bdesc(sb + p.off_bh + (uint32_t)(H / 2 / 8) * p.sbo_bh, p.sbo_bh);
 
+  // predict: the rows of the slot's next tile are bulk-copied (TMA engine) into
+  // a per-slot shared-memory buffer one tile ahead (issued with the L1 that
+  // frees it); partial tiles, or an x pointer that is not 16-byte aligned,
+  // read global memory directly (sweep_kernel3's prologue)
+  uint8_t* xs = smem + p.smem_x + s * p.x_tile_bytes;
+  uint64_t* xbar = &bars[9 + s];
+  uint32_t phx = 0;
+  uint64_t x_next = 0;  // tile whose rows the next L1 issue prefetches
+  auto x_full = [&](uint64_t tl_) { return p.x_tma != 0u && p.begin + (tl_ + 1) * TILE_M <= p.end; };
+  auto x_issue = [&](uint64_t tl_) {  // one thread
+    if (tl_ < p.num_tiles && x_full(tl_)) {
+      mbar_arrive_expect_tx(xbar, p.x_tile_bytes);
+      bulk_g2s(xs, reinterpret_cast<const uint8_t*>(p.x + (p.begin + tl_ * TILE_M) * p.P), p.x_tile_bytes, xbar);
+    }
+  };
+
   // every warp of the slot is done with its TMEM writes / reads and A0 stores
   // -> one elected lane issues the phase (0: L1, 1: L2a, 2: L2b) and commits
   auto issue = [&](int phase) {
@@ -141,6 +163,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
       tc_fence_after();
       if (elect_one()) {
         if (phase == 0) {
+          if (PRED) x_issue(x_next);  // the A0 tile holds the rows now: the buffer is free
           umma_f16_ss(dslot, d_a0, d_b1, idesc_full, 0u);
         } else {
           const uint64_t bd = phase == 1 ? d_b2a : d_b2b;
@@ -153,10 +176,21 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
       __syncwarp();
     }
   };
-  auto store_a0 = [&](const uint32_t (&D)[MAXG], uint64_t Ir) {
+  // the layer-1 operand row of tile tl_ (index Ir): decoded, or (PRED) the row's raw values
+  auto store_a0 = [&](const uint32_t (&D)[MAXG], uint64_t tl_, uint64_t Ir) {
     A0Regs a0;
-    if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC>(p, slut, D, a0);
-    if (FM != MODE_TOPK) a0_dump<false>(p, mode, a0, Ir);
+    if constexpr (PRED) {
+      if (x_full(tl_)) {
+        mbar_wait(xbar, phx);
+        phx ^= 1u;
+        make_a0_row<PREC, true>(p, reinterpret_cast<const float*>(xs) + row * p.P, a0);
+      } else {
+        make_a0_predict<PREC>(p, Ir < p.end ? Ir : p.begin, a0);
+      }
+    } else {
+      if (SPG == 4) make_a0_sweep4(p, slut, D, a0); else make_a0_sweep<PREC>(p, slut, D, a0);
+    }
+    if (FM != MODE_TOPK && !PRED) a0_dump<false>(p, mode, a0, Ir);
     st_shared_v4(a0_st, a0.hi[0], a0.hi[1], a0.hi[2], a0.hi[3]);
     st_shared_v4(a0_st + 128u, a0.hi[4], a0.hi[5], a0.hi[6], a0.hi[7]);
     fence_proxy_async_smem();
@@ -165,18 +199,23 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
   auto emit = [&](float t, uint64_t Ir) {
     const bool valid = Ir < p.end;
     if (mode == MODE_TOPK) topk_offer(ts, mycand, ncand, valid, t, Ir, p.k, lane);
-    else if (valid && mode == MODE_DENSE) p.t_dense[Ir - p.begin] = t;
+    else if (valid && (mode == MODE_DENSE || mode == MODE_PREDICT)) p.t_dense[Ir - p.begin] = t;
   };
 
   uint64_t tile = (uint64_t)blockIdx.x * NSLOT + s;
   uint64_t I = p.begin + tile * TILE_M + row;
   const uint64_t dI = (uint64_t)p.dTiles * TILE_M;
   uint32_t D[MAXG];
-  init_digits_n<NG>(p.R, I, D);
+  if (!PRED) init_digits_n<NG>(p.R, I, D);
   uint32_t ph = 0;
   mbar_wait(&bars[0], 0);
+  if (PRED) {
+    if (wq == 0 && elect_one()) x_issue(tile);
+    __syncwarp();
+    x_next = tile + p.dTiles;
+  }
   if (tile < p.num_tiles) {
-    store_a0(D, I);
+    store_a0(D, tile, I);
     issue(0);  // L1 of the first tile
   }
   // tile t-1 carried into iteration t: half a's sum, half b's accumulators
@@ -225,8 +264,9 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8(const __grid_constant__ 
       }
     }
     if (has_next) {
-      odometer_step_n<NG>(p.R, p.dD, D);
-      store_a0(D, In);
+      if (!PRED) odometer_step_n<NG>(p.R, p.dD, D);
+      store_a0(D, tile + p.dTiles, In);
+      if (PRED) x_next = tile + 2 * (uint64_t)p.dTiles;
     }
     if (tr) trace_ev(p, s, jr, 3);
     // ---- L2a done: load half a, release it to L2b, FP32 half a in the L2b shadow
