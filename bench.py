@@ -288,6 +288,13 @@ def main():
     wl = workloads.WORKLOADS[args.workload]
     precision = args.precision or wl.precision
     if args.gpus > 1 and "RANK" not in os.environ and args.impl == "ours":
+        if not args.dry_run:
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:  # one process per GPU: refuse rather than share devices
+                print(json.dumps({"error": f"--gpus {args.gpus} requested, {have} CUDA device(s) visible",
+                                  "n_gpus": args.gpus}), flush=True)
+                sys.exit(2)
         sys.exit(relaunch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
