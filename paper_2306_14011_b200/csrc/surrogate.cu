@@ -680,6 +680,7 @@ surr_status plan(surrogate* h, uint64_t begin, uint64_t end, uint32_t k, int mod
     p.ens_gm = L->ki.w_mult;
     p.ens_e = E;
     for (uint32_t e = 0; e < E && e < 16; ++e) p.ens_c[e] = h->members[e].c_out;
+    for (uint32_t e = 0; e < E && e < 8; ++e) memcpy(p.ens_w[e], h->members[e].fin_w, sizeof p.ens_w[e]);
     p.inv_e = 1.0f / (float)E;
   }
   const KParams& s = h->sp;

@@ -118,13 +118,15 @@ struct KParams {
   // each member's de-standardisation constant, shared-memory weight region
   uint32_t ens_gm, ens_e;
   float ens_c[16];
+  alignas(16) float ens_w[8][128];  // members' final-layer w' = y_scale w / 2 (uniform LDCU.128 operands)
   // debug timeline (CTA 0 only): trace[ev] = clock64 of event ev, or null
   unsigned long long* trace;
   uint32_t trace_n;
   uint32_t variant;  // schedule variant (development A/B switch, env SURR_VARIANT; 0 = default)
 };
 
-static_assert(offsetof(KParams, fin_w) % 16 == 0 && offsetof(KParams, fin_nb) % 16 == 0,
+static_assert(offsetof(KParams, fin_w) % 16 == 0 && offsetof(KParams, fin_nb) % 16 == 0 &&
+                  offsetof(KParams, ens_w) % 16 == 0,
               "epilogue constants must stay 16-byte aligned in the parameter bank (LDCU.128)");
 
 // Ensemble accumulator value of row I, loaded at the start of a tile so that

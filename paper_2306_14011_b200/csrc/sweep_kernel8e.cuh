@@ -23,24 +23,26 @@
 
 namespace surr {
 
-// final-layer FFMA2 steps with the member's weights w' = y_scale w / 2 from its
-// shared-memory image, four per broadcast LDS.128 (the accumulator order is
-// final_compute's, so t is bitwise the single-net path's)
+// final-layer FFMA2 steps with member mi's weights w' = y_scale w / 2 from the
+// parameter bank (p.ens_w).  mi is a compile-time constant at every call (the
+// member loop is unrolled and the CTA rank selects between two calls), so the
+// weights are uniform LDCU.128 operands as in the single-net kernel; with a
+// run-time member index they compiled to per-thread LDC (-3.7 %), and from the
+// shared-memory image as broadcast LDS.128 they cost 11 % (same-box A/B,
+// DESIGN section 7).  The accumulator order is final_compute's, so t is
+// bitwise the single-net path's.
 template <int NC>
-__device__ __forceinline__ float final_compute_c(const float* w, const uint32_t (&v)[64], int n0) {
+__device__ __forceinline__ float final_compute_k(const KParams& p, uint32_t mi, const uint32_t (&v)[64], int n0) {
   uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-  for (int j = 0; j < NC; j += 4) {
-    const float4 w4 = *reinterpret_cast<const float4*>(w + n0 + j);
-    const uint64_t wa = pack2(w4.x, w4.y), wb = pack2(w4.z, w4.w);
-    acc[0] = ffma2(wa, pack2(__uint_as_float(v[j]), __uint_as_float(v[j + 1])), acc[0]);
-    acc[2] = ffma2(wa, pack2(fabsf(__uint_as_float(v[j])), fabsf(__uint_as_float(v[j + 1]))), acc[2]);
-    acc[1] = ffma2(wb, pack2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])), acc[1]);
-    acc[3] = ffma2(wb, pack2(fabsf(__uint_as_float(v[j + 2])), fabsf(__uint_as_float(v[j + 3]))), acc[3]);
+  for (int j = 0; j < NC; j += 2) {
+    const uint64_t w2 = pack2(p.ens_w[mi][n0 + j], p.ens_w[mi][n0 + j + 1]);
+    const float x0 = __uint_as_float(v[j]), x1 = __uint_as_float(v[j + 1]);
+    acc[(j >> 1) & 1] = ffma2(w2, pack2(x0, x1), acc[(j >> 1) & 1]);
+    acc[2 + ((j >> 1) & 1)] = ffma2(w2, pack2(fabsf(x0), fabsf(x1)), acc[2 + ((j >> 1) & 1)]);
   }
   return fin_sum(acc);
 }
-
 template <int H, int SPG, int PREC, int GM>
 __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__ KParams p, int mode) {
   constexpr int NG = K0 / SPG;
@@ -132,7 +134,6 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
   const uint64_t d_b2a = make_bdesc(sb + p.off_bh, p.sbo_bh);
   const uint64_t d_b2b = make_bdesc(sb + p.off_bh + (uint32_t)(H / 2 / 8) * p.sbo_bh, p.sbo_bh);
   const uint64_t d_step = (uint64_t)(p.w_bytes >> 4);
-  auto fin_w = [&](uint32_t m) { return reinterpret_cast<const float*>(smem + m * p.w_bytes + p.off_fin); };
 
   auto issue = [&](int phase, uint32_t m) {
     tc_fence_before();
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
   for (; tile < p.num_tiles; tile += p.dTiles) {
     const uint64_t In = I + dI;
     const bool has_next = tile + p.dTiles < p.num_tiles;
-#pragma unroll 1
+#pragma unroll  // compile-time member index: uniform final-layer weight operands
     for (uint32_t m = 0; m < (uint32_t)GM; ++m) {
       const bool last_m = m + 1 == (uint32_t)GM;
       // ---- L1(unit) done -> epilogue 1 in place
@@ -268,7 +269,8 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
         uint32_t v[64];
         final_load<H / 2>(dcol + H / 2, v);
         issue(2, m);
-        pa = final_compute_c<H / 2>(fin_w(m), v, 0);
+        // (blockIdx.x & 1 = this CTA's rank in its cluster of two, members rank GM + m)
+        pa = (blockIdx.x & 1u) ? final_compute_k<H / 2>(p, GM + m, v, 0) : final_compute_k<H / 2>(p, m, v, 0);
       }
       // ---- L2b done: half b, next unit's L1 (same A0 with the next member, or the next tile's)
       mbar_wait(&bars[4 + s], ph);
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel8e(const __grid_constant__
         final_load<H / 2>(dcol + H / 2, v);
         if (!last_m) issue(0, m + 1);
         else if (has_next) issue(0, 0);
-        pdot = pa + final_compute_c<H / 2>(fin_w(m), v, H / 2);
+        pdot = pa + ((blockIdx.x & 1u) ? final_compute_k<H / 2>(p, GM + m, v, H / 2) : final_compute_k<H / 2>(p, m, v, H / 2));
       }
       pm = m;
       pI = I;

@@ -25,14 +25,24 @@ def _sanitizer():
     return exe
 
 
+def _run(cmd):
+    """Run cmd under compute-sanitizer; skip when the GPU pool refuses the tool
+    (some pools wrap compute-sanitizer and close it: it exits without running
+    the target and says so)."""
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    out = res.stdout + res.stderr
+    if "sanitize_target done" not in out and "closed on this pool" in out:
+        pytest.skip("compute-sanitizer refused on this GPU pool: " + out.strip().splitlines()[-1][:200])
+    return res, out
+
+
 @pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
 def test_compute_sanitizer_clean(tool):
     need_gpu()
     cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "97", "--print-limit", "20"]
     if tool == "memcheck":
         cmd += ["--leak-check", "no"]
-    res = subprocess.run(cmd + [sys.executable, TARGET], capture_output=True, text=True, timeout=1800)
-    out = res.stdout + res.stderr
+    res, out = _run(cmd + [sys.executable, TARGET])
     assert "sanitize_target done" in out, out[-4000:]
     assert res.returncode == 0 and "ERROR SUMMARY: 0 errors" in out, out[-4000:]
 
@@ -51,8 +61,7 @@ LOCKED = {"warp_merge", "upper_bound_recs_fwd", "lower_bound_recs", "topk_offer"
 def test_compute_sanitizer_racecheck_only_lock_protected_merge():
     need_gpu()
     cmd = [_sanitizer(), "--tool", "racecheck", "--print-limit", "100000", sys.executable, TARGET]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
-    out = res.stdout + res.stderr
+    res, out = _run(cmd)
     assert "sanitize_target done" in out, out[-4000:]
     fns = set(re.findall(r"access at (?:surr::)?([A-Za-z_0-9]+)\(", out))
     assert fns <= LOCKED, f"racecheck hazards outside the lock-protected top-k merge: {sorted(fns - LOCKED)}"
